@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark of the lossless homomorphic compression hot path on B200.
+
+One step = Alg. 1 end to end for the configured workload: every
+rank compresses the gradients of the workers it holds (W workers spread over N
+GPUs), the sketches are aggregated (on one GPU with sketch_aggregate, across
+GPUs with the NVLink P2P sketch_allreduce), and every rank decodes the aggregate
+into the dense sum.  Metric (BASELINE.json): aggregated gradient elements/s =
+d / T_step, d counted once however many workers (footnote P:L367).
+
+    python bench.py [--gpus N --steps K --warmup W --config ncf]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference ...     # the CPU oracle, timed as it stands
+
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from lhc_inputs import config as workload_config  # noqa: E402
+
+METRIC = "aggregated gradient elements/s (compress+aggregate+decode) at 1/2/4/8 B200"
+UNIT = "elements/s"
+SEED = 0x1DC0DE
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="ncf", help="tiny|ncf|lstm|bert|vgg")
+    ap.add_argument("--density", type=float, default=None)
+    ap.add_argument("--workers", type=int, default=None)
+    ap.add_argument("--gamma", type=float, default=1.30)
+    ap.add_argument("--law", default="gauss")
+    ap.add_argument("--fuse-local", action="store_true",
+                    help="compress a rank's workers straight into one sketch (no per-worker sketches)")
+    ap.add_argument("--comm", choices=["p2p", "nccl"], default="p2p")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
+    ap.add_argument("--phases", action="store_true", help="also print per-phase times (stderr)")
+    return ap.parse_args()
+
+
+def workload(args):
+    over = {"law": args.law}
+    if args.density is not None:
+        over["density"] = args.density
+    if args.workers is not None:
+        over["workers"] = args.workers
+    return workload_config(args.config, **over)
+
+
+# --------------------------------------------------------------------- clocks --
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# -------------------------------------------------------------- reference arm --
+
+def run_reference(args, wl, rank):
+    """The CPU oracle (oracle/, plain single-threaded C) timed as it stands."""
+    if rank != 0:
+        return None
+    import oracle
+
+    from paper_2402_07529_b200.sizing import size_workload
+
+    oracle.build()
+    target = max(5.0, 150.0 / max(1, args.steps + args.warmup))
+    # calibrate on a small prefix, then size the per-step sample to ~target seconds
+    frac = 1.0
+    cal = sample_workload(wl, 1 / 64)
+    t_cal = oracle_step(oracle, cal, size_workload, args.gamma)
+    est_full = t_cal * 64
+    if est_full > target:
+        frac = max(1 / 64, target / est_full)
+    sub = sample_workload(wl, frac)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t = oracle_step(oracle, sub, size_workload, args.gamma)
+        if s >= args.warmup:
+            times.append(t)
+    T = sum(times) / len(times)
+    value = sub.d / T
+    sample = (f"{sub.workers} workers x d={sub.d} ({frac:.3f} of {wl.name}'s d={wl.d}), "
+              f"same density/structure/sizing rule; full pipeline per step")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": T * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl.name, "d": wl.d, "density": wl.density,
+                       "workers": wl.workers, "structure": wl.structure},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+def sample_workload(wl, frac):
+    from lhc_inputs import Workload
+
+    d = max(4096, int(wl.d * frac))
+    kw = dict(wl.__dict__)
+    kw["d"] = d
+    return Workload(**kw)
+
+
+def oracle_step(oracle, wl, size_workload, gamma):
+    xs = [wl.dense(w) for w in range(wl.workers)]
+    s = size_workload(wl.d, wl.density, wl.workers, gamma=gamma)
+    p = oracle.params(wl.d, s.m, s.c, 3, 0, 1024, SEED)
+    t0 = time.perf_counter()
+    oracle.pipeline(p, xs)
+    return time.perf_counter() - t0
+
+
+# ------------------------------------------------------------------- our arm --
+
+def main():
+    args = parse()
+    wl = workload(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+
+    if args.impl == "reference":
+        line = run_reference(args, wl, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_07529_b200 as lhc
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lhc.lib()
+
+    sz = lhc.size_workload(wl.d, wl.density, wl.workers, gamma=args.gamma)
+    p = lhc.params(wl.d, sz.m, sz.c, 3, 0, 1024, SEED)
+    cap = min(wl.d, int(sz.n_cand_expected * 1.25) + 4096)
+    my_workers = [w for w in range(wl.workers) if w % world == rank]
+
+    # inputs resident in HBM (generated on the host with the shared seeded recipe)
+    host = [wl.dense(w) for w in my_workers]
+    xs = [torch.from_numpy(x).to(dev) for x in host]
+
+    comm = None
+    if world > 1 and args.comm == "p2p":
+        comm = lhc.PeerComm(p)
+    run = lhc.LosslessAllReduce(p, cap, local_workers=len(xs), per_worker=not args.fuse_local,
+                                comm=comm, device=dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    nccl_state = {}
+
+    def nccl_allreduce():
+        # baseline exchange: NCCL sum of counters + all-gather of bitmaps + OR
+        # (NCCL has no bitwise-OR reduction); torch ops, not the product path
+        sk = run.sketch
+        dist.all_reduce(sk.counters)
+        if "g" not in nccl_state:
+            nccl_state["g"] = torch.empty((world, sk.bitmap.numel()), dtype=torch.int32, device=dev)
+        g = nccl_state["g"]
+        dist.all_gather_into_tensor(g, sk.bitmap)
+        out = g[0].clone()
+        for r in range(1, world):
+            out.bitwise_or_(g[r])
+        sk.bitmap.copy_(out)
+
+    # instrumented step: CUDA events around each phase on the launching stream
+    def step(ev=None, launches=None):
+        def mark(name):
+            if ev is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                ev.append((name, e))
+
+        def cnt():
+            if launches is not None:
+                launches[0] += lhc.last_launch_count()
+
+        mark("start")
+        if run.per_worker:
+            for sk, x in zip(run.worker_sketches, xs):
+                sk.clear()
+                mark("compress0")
+                sk.compress(x)
+                cnt()
+                mark("compress1")
+            lhc.aggregate(p, run.worker_sketches, run.sketch)
+            cnt()
+            mark("aggregate")
+        else:
+            run.sketch.clear()
+            for x in xs:
+                mark("compress0")
+                run.sketch.compress(x)
+                cnt()
+                mark("compress1")
+            mark("aggregate")
+        if world > 1:
+            if comm is not None:
+                comm.allreduce()
+                cnt()
+            else:
+                nccl_allreduce()
+        mark("allreduce")
+        run.decoder(run.sketch)
+        cnt()
+        mark("decode")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    n_warm = max(3, args.warmup)  # timing rule: at least 3 untimed warm-up steps
+    for _ in range(n_warm):
+        step()
+    barrier()
+
+    # ---- timed region: K steps, per-step events, L2 flushed between steps ----
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    per_step = []
+    phase = {"compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "decode": 0.0}
+    compress_launch_ms = []
+    launches = [0]
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        ev = []
+        step(ev, launches)
+        per_step.append(ev)
+    barrier()
+    clocks.stop()
+    total_ms = 0.0
+    for ev in per_step:
+        t = dict()
+        st = ev[0][1]
+        total_ms += st.elapsed_time(ev[-1][1])
+        prev = st
+        for name, e in ev[1:]:
+            dt = prev.elapsed_time(e)
+            if name == "compress1":
+                compress_launch_ms.append(dt)
+                phase["compress"] += dt
+            elif name in phase:
+                phase[name] += dt
+            prev = e
+        del t
+    ms = total_ms / args.steps
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+
+    stats = run.decoder.read_stats()
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        pinned = [torch.from_numpy(x).pin_memory() for x in host]
+        out_host = torch.empty(p.d, dtype=torch.float32).pin_memory()
+        dev_in = [torch.empty_like(x) for x in xs]
+        h2d = sum(x.numel() * 4 for x in pinned)
+        d2h = out_host.numel() * 4
+
+        def e2e_step():
+            for h, d_ in zip(pinned, dev_in):
+                d_.copy_(h, non_blocking=True)
+            run.step(dev_in)
+            out_host.copy_(run.decoder.dense, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        n_e2e = max(3, min(args.steps, 10))
+        e0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        e_ms = torch.tensor([e0.elapsed_time(e1) / n_e2e], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": wl.d / (float(e_ms.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": float(e_ms.item()),
+               "path": "pinned host x_w -> H2D -> LosslessAllReduce.step -> dense sum D2H"}
+        if not np.isfinite(e2e["value"]):
+            e2e = None
+
+    # ---- roofline of the dominant kernel (compress) ----
+    import json as _json
+
+    peaks = {}
+    try:
+        peaks = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    avg_compress_ms = sum(compress_launch_ms) / max(1, len(compress_launch_ms))
+    bytes_compress = 4 * wl.d + (int(p.m) // 8 + 4 * int(p.c))  # read x_w, write the sketch
+    achieved = bytes_compress / (avg_compress_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_compress_dense", "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "bytes_per_launch": bytes_compress, "avg_launch_us": avg_compress_ms * 1e3,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ref = run_reference(argparse.Namespace(steps=1, warmup=0, gamma=args.gamma), wl, 0)
+        cpu = ref["cpu_baseline"] if ref else None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": wl.d / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": n_warm, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": wl.name, "d": wl.d, "density": wl.density,
+                       "workers": wl.workers, "structure": wl.structure, "law": wl.law,
+                       "k": 3, "L": 1024, "m": int(p.m), "c": int(p.c), "gamma": args.gamma,
+                       "sketch_bytes": int(p.m) // 8 + 4 * int(p.c),
+                       "per_worker_sketches": run.per_worker,
+                       "comm": ("p2p" if comm is not None else "nccl") if world > 1 else "none",
+                       "l2": "flushed (256 MB write) between timed steps, outside the events"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches[0],
+            "clocks": clocks.summary(),
+            "phases_ms_per_step": {k: v / args.steps for k, v in phase.items()},
+            "decode": stats,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

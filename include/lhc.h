@@ -1,0 +1,182 @@
+/*
+ * lhc.h — C ABI of the B200 (sm_100a) hot path of lossless homomorphic gradient
+ * compression (arXiv 2402.07529, "Accelerating Distributed Deep Learning using
+ * Lossless Homomorphic Compression").  PAPER.md lines are cited as P:L<n>.
+ *
+ * Algorithm 1: every worker compresses its gradient X into
+ * S(X) = [Y, B] (Count Sketch Y + Bloom-filter index B), the aggregation API
+ * makes Y <- sum Y and B <- OR B without decompressing, and every
+ * worker recovers sum X by peeling and estimation.
+ *
+ * Conventions for every call below
+ *   - All array pointers are DEVICE pointers unless stated otherwise; every
+ *     compute call is asynchronous and stream-ordered on `stream` (a
+ *     cudaStream_t passed as void*; NULL = the legacy default stream).
+ *   - The caller owns every buffer.  The library allocates nothing except the
+ *     small state object of lhc_comm_create.
+ *   - Shape and argument errors are detected synchronously on the host and
+ *     returned as LHC_EINVAL before anything is launched.  Data-dependent
+ *     conditions (candidate overflow, a stalled peel) are reported through the
+ *     device-resident lhc_stats, never by a host synchronisation (Alg. 1 estimates
+ *     the unpeeled parameters instead of failing).  A failed launch
+ *     returns LHC_ECUDA; lhc_last_error() gives the message (thread-local).
+ *   - Two sketches can be merged only if their lhc_params are identical
+ *     (merge-compatibility); the caller enforces it.
+ *   - Bit b of a Bloom filter is bit (b & 31) of 32-bit word (b >> 5).
+ *   - Alignment: x, counters, bitmaps, out_dense and the workspace must be
+ *     16-byte aligned (LHC_EINVAL otherwise).
+ *   - Calls on distinct buffers are thread-safe.
+ *
+ * Layout (§3.4 "Locality Optimization"): coordinate p of the
+ * gradient is (input row i = p / L, column t = p % L).  Each input row i and
+ * probe j has one (row, bias, sign) triple (reading R4: "each batch shares the
+ * same index"); probe j of the Count Sketch lives in partition j of Y (rows
+ * [j*S_Y, (j+1)*S_Y), S_Y = c/(k*L); reading R2: "three different indexes"),
+ * probe j of the Bloom filter in partition j of B (S_B = m/(k_bloom*L)):
+ *   cell_j(p) = row_j(i)*L + (t + bias_j(i)) mod L          (Y: fp32 cells)
+ *   bit_j(p)  = rowB_j(i)*L + (t + biasB_j(i)) mod L        (B: bits)
+ * The hash (reading R1; the paper gives none) is
+ *   mix64(z) = SplitMix64 finalizer
+ *   H(seed,dom,j,i) = mix64(seed ^ mix64(((dom<<56)|(j<<48)|i) + 0x9E3779B97F4A7C15))
+ *   row = j*S + ((H>>32)*S >> 32), bias = H & (L-1), sign = bit16(H) ? -1 : +1,
+ * dom 0 = Count Sketch (S = S_Y), dom 1 = Bloom filter (S = S_B).
+ */
+#ifndef LHC_H
+#define LHC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Sizes of one sketch S(X) = [Y, B] (Alg. 1). */
+typedef struct lhc_params {
+    uint32_t d;        /* gradient coordinates, 1 <= d < 2^32 (paper: N)            */
+    uint64_t m;        /* Bloom-filter bits, multiple of k_bloom*L, m/L < 2^32     */
+    uint64_t c;        /* Count Sketch cells, multiple of k*L, c < 2^32 (size of Y) */
+    uint32_t k;        /* Count Sketch hashes, 1..8 (paper: 3)                      */
+    uint32_t k_bloom;  /* Bloom probes, 0..8; 0 means k (paper: log 1/eps)         */
+    uint32_t L;        /* batch width, power of two in [32, 1024] (paper: c=1024)  */
+    uint64_t seed;     /* hash seed; every rank must use the same one                       */
+} lhc_params;
+
+/* Device-resident decode statistics (§4.1.1 metrics). */
+typedef struct lhc_stats {
+    uint64_t n_cand;   /* candidates n_c returned by the Bloom query (may exceed cap)        */
+    uint64_t n_peeled; /* candidates recovered exactly by peeling ("recovery rate" numerator) */
+    uint32_t rounds;   /* synchronous peeling rounds that peeled something ("iterations")    */
+    int32_t success;   /* 1 iff n_peeled == n_cand and no overflow (lossless)        */
+    int32_t overflow;  /* 1 iff n_cand > cap_cand: outputs truncated, nothing peeled         */
+    uint32_t _reserved;
+} lhc_stats;
+
+enum {
+    LHC_OK = 0,
+    LHC_EINVAL = 1,    /* invalid argument, shape or alignment                         */
+    LHC_ECAPACITY = 2, /* workspace too small                                          */
+    LHC_ECUDA = 3,     /* a CUDA call or launch failed                                 */
+    LHC_ECOMM = 4      /* peer mapping / IPC failure                                   */
+};
+
+/* ---- host helpers (synchronous, no device work) ------------------------- */
+
+/* LHC_OK if the parameters satisfy every constraint listed in lhc_params. */
+int lhc_validate(const lhc_params* p);
+/* Human-readable text of the last error on the calling thread (never NULL). */
+const char* lhc_last_error(void);
+/* Number of 32-bit words of the Bloom filter: m / 32. */
+uint64_t lhc_bitmap_words(const lhc_params* p);
+/* Bytes of device workspace sketch_decompress needs for at most cap_cand
+ * candidates (0 on invalid parameters). */
+size_t lhc_decompress_workspace(const lhc_params* p, uint64_t cap_cand);
+
+/* ---- Phase I: compression (Alg. 1) ---------------------------- */
+
+/* Seeded hash kernel: writes the per-input-row map of domain dom (0 = Count
+ * Sketch, 1 = Bloom filter) for input rows [0, n_rows):
+ *   out[2*(i*kk + j)]     = row_j(i)       (absolute row of Y or B, partition j)
+ *   out[2*(i*kk + j) + 1] = bias_j(i) | (sign_j(i) < 0) << 31
+ * with kk = k (dom 0) or k_bloom (dom 1).  out holds 2*n_rows*kk u32. */
+int sketch_hash_rows(const lhc_params* p, uint32_t dom, uint64_t n_rows, uint32_t* out,
+                     void* stream);
+
+/* Zero a sketch (bitmap: m/32 words, counters: c floats) before compression. */
+int sketch_clear(const lhc_params* p, uint32_t* bitmap, float* counters, void* stream);
+
+/* Compress a dense fp32 gradient x[d] (Alg. 1 Phase I; Count Sketch P:L175,
+ * Bloom filter P:L230, batched layout P:L262).  Every coordinate with
+ * x[p] != 0.0f (IEEE compare: -0.0 counts as zero) sets its k_bloom bits in
+ * bitmap[m/32] (bitwise OR) and adds sign_j*x[p] to its k cells of
+ * counters[c] (fp32 atomic add, round-to-nearest; order-dependent rounding).
+ * ACCUMULATES: compressing several gradients into one sketch yields the
+ * aggregate sketch of their sum (the homomorphism of P:L137).  nnz_out
+ * (device, nullable) is incremented by the number of nonzeros. */
+int sketch_compress(const lhc_params* p, const float* x, uint32_t* bitmap, float* counters,
+                    unsigned long long* nnz_out, void* stream);
+
+/* Same from a COO gradient: idx[nnz] (each < d, distinct), val[nnz].  Every
+ * listed entry is inserted, including val == 0 (the index describes the listed
+ * support).  Accumulates like sketch_compress. */
+int sketch_compress_coo(const lhc_params* p, uint64_t nnz, const uint32_t* idx,
+                        const float* val, uint32_t* bitmap, float* counters, void* stream);
+
+/* ---- aggregation (Alg. 1: Y <- sum Y, B <- OR B) ---------------- */
+
+/* Single-GPU aggregation of n_in sketches (e.g. workers simulated on one GPU):
+ * out_bitmap = OR_r bitmaps[r], out_counters = sum_r counters[r] (fp32, summed
+ * in ascending r).  bitmaps/counters are HOST arrays of n_in device pointers;
+ * out may alias bitmaps[0]/counters[0]. */
+int sketch_aggregate(const lhc_params* p, int n_in, const uint32_t* const* bitmaps,
+                     const float* const* counters, uint32_t* out_bitmap, float* out_counters,
+                     void* stream);
+
+/* Multi-GPU aggregation over NVLink peer memory (one process per GPU).
+ * The communication buffer of every rank holds [bitmap | counters | signals]
+ * at the offsets lhc_comm_layout returns; compress straight into it.
+ * lhc_ipc_handle exports a buffer (CUDA IPC handle, 64 bytes, plus the offset
+ * of dev_ptr inside its allocation); the caller exchanges them (e.g. with
+ * torch.distributed.all_gather_object) and passes all world handles/offsets to
+ * lhc_comm_create, which maps the peers' buffers.  sketch_allreduce then makes
+ * every rank's [bitmap | counters] the OR / sum over all ranks, in place, with
+ * a two-shot reduce-scatter + all-gather over NVLink and system-scope flag
+ * barriers (counters summed in ascending rank order: identical on all ranks). */
+typedef struct lhc_comm lhc_comm;
+int lhc_comm_layout(const lhc_params* p, size_t* bitmap_off, size_t* counters_off,
+                    size_t* signals_off, size_t* total_bytes);
+int lhc_ipc_handle(const void* dev_ptr, void* handle_out /*64 bytes*/, uint64_t* offset_out);
+int lhc_comm_create(int rank, int world, const void* handles /*world*64 bytes, host*/,
+                    const uint64_t* offsets /*world, host*/, void* local_buf, size_t buf_bytes,
+                    const lhc_params* p, lhc_comm** out);
+int sketch_allreduce(lhc_comm* comm, void* stream);
+void lhc_comm_destroy(lhc_comm* comm);
+
+/* ---- Phase II: recovery (Alg. 1) ----------------------------- */
+
+/* Decode an aggregated sketch [bitmap, counters] (not modified):
+ *   1. Bloom query over all d coordinates (a coordinate is a candidate
+ *      iff all its k_bloom bits are set); the n_c candidates are written in
+ *      ascending order to out_idx[cap_cand]; slot s names out_idx[s].
+ *   2. Peeling: synchronous rounds; every cell holding exactly one
+ *      unpeeled candidate recovers it (val = sign * residual) and the value is
+ *      subtracted from the candidate's other cells.
+ *   3. Estimation of candidates peeling did not reach: median over j
+ *      of sign_j * residual (reading R11).
+ *   out_val[s], out_peeled[s] (1 = recovered exactly, 0 = estimated) for
+ *   s < n_c; out_dense[d] (nullable) = value at candidates, exactly 0 elsewhere.
+ * ws: lhc_decompress_workspace(p, cap_cand) bytes.  stats: device lhc_stats.
+ * If n_c > cap_cand, stats.overflow = 1 and the outputs are undefined. */
+int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* counters,
+                      void* ws, size_t ws_bytes, uint64_t cap_cand, uint32_t* out_idx,
+                      float* out_val, uint8_t* out_peeled, float* out_dense, lhc_stats* stats,
+                      void* stream);
+
+/* Number of kernel launches the last successful call of each entry point made
+ * on this thread (bench accounting of `gpu_launches`). */
+int lhc_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LHC_H */

@@ -1,0 +1,68 @@
+// aggregate.cu — single-GPU homomorphic aggregation (Alg. 1 comment, P:L148-149:
+// "Y <- sum Y and B <- OR B"): a streaming, 128-bit vectorised OR over the
+// Bloom filters and fp32 sum over the Count Sketches of n_in sketches.
+#include "launch.h"
+
+namespace lhc {
+
+constexpr int kAggMaxIn = 16;
+
+struct AggArgs {
+    const uint32_t* b[kAggMaxIn];
+    const float* y[kAggMaxIn];
+    int n;
+    int accumulate;  // 1: also add/OR the current output (chunked n_in > kAggMaxIn)
+};
+
+__global__ void __launch_bounds__(256)
+k_aggregate(AggArgs A, uint64_t n_words, uint64_t c, uint32_t* ob, float* oy) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // Bloom filters: 16-byte groups of words, scalar tail
+    const uint64_t nb4 = n_words / 4;
+    for (uint64_t u = tid; u < nb4; u += stride) {
+        uint4 acc = A.accumulate ? reinterpret_cast<const uint4*>(ob)[u] : make_uint4(0, 0, 0, 0);
+        for (int r = 0; r < A.n; r++) {
+            uint4 v = __ldcs(reinterpret_cast<const uint4*>(A.b[r]) + u);
+            acc.x |= v.x; acc.y |= v.y; acc.z |= v.z; acc.w |= v.w;
+        }
+        reinterpret_cast<uint4*>(ob)[u] = acc;
+    }
+    for (uint64_t w = nb4 * 4 + tid; w < n_words; w += stride) {
+        uint32_t acc = A.accumulate ? ob[w] : 0u;
+        for (int r = 0; r < A.n; r++) acc |= A.b[r][w];
+        ob[w] = acc;
+    }
+    // Count Sketches (c is a multiple of k*L >= 32): summed in ascending r
+    const uint64_t nc4 = c / 4;
+    for (uint64_t u = tid; u < nc4; u += stride) {
+        float4 acc = A.accumulate ? reinterpret_cast<const float4*>(oy)[u]
+                                  : __ldcs(reinterpret_cast<const float4*>(A.y[0]) + u);
+        for (int r = A.accumulate ? 0 : 1; r < A.n; r++) {
+            float4 v = __ldcs(reinterpret_cast<const float4*>(A.y[r]) + u);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        reinterpret_cast<float4*>(oy)[u] = acc;
+    }
+}
+
+void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* const* bitmaps,
+                      const float* const* counters, uint32_t* out_bitmap, float* out_counters,
+                      cudaStream_t s) {
+    const uint64_t units = std::max<uint64_t>(n_words / 4, c / 4);
+    const uint32_t blocks =
+        (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((units + 255) / 256, (uint64_t)num_sms() * 8));
+    for (int r0 = 0; r0 < n_in; r0 += kAggMaxIn) {
+        AggArgs A{};
+        A.n = std::min(kAggMaxIn, n_in - r0);
+        A.accumulate = r0 > 0;
+        for (int r = 0; r < A.n; r++) {
+            A.b[r] = bitmaps[r0 + r];
+            A.y[r] = counters[r0 + r];
+        }
+        k_aggregate<<<blocks, 256, 0, s>>>(A, n_words, c, out_bitmap, out_counters);
+        count_launch();
+    }
+}
+
+}  // namespace lhc

@@ -1,0 +1,224 @@
+// api.cu — the C ABI of include/lhc.h: host-side validation, workspace layout and
+// launch sequencing.  All compute happens in the kernels of compress.cu,
+// aggregate.cu, query.cu, peel.cu and comm.cu; nothing here touches data.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "launch.h"
+
+namespace lhc {
+
+static thread_local char g_err[512] = "no error";
+static thread_local int g_launches = 0;
+
+void count_launch(int n) { g_launches += n; }
+void reset_launches() { g_launches = 0; }
+
+int num_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && cached[dev]) return cached[dev];
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    if (dev < 64) cached[dev] = n;
+    return n;
+}
+
+int set_error(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+static int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(LHC_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return LHC_OK;
+}
+
+static uint32_t ilog2(uint32_t x) {
+    uint32_t r = 0;
+    while ((1u << r) < x) r++;
+    return r;
+}
+
+int validate(const lhc_params* p) {
+    if (!p) return set_error(LHC_EINVAL, "params is NULL");
+    if (p->d == 0) return set_error(LHC_EINVAL, "d must be >= 1");
+    if (p->k == 0 || p->k > (uint32_t)kMaxK) return set_error(LHC_EINVAL, "k must be in [1, 8]");
+    if (p->k_bloom > (uint32_t)kMaxK) return set_error(LHC_EINVAL, "k_bloom must be in [0, 8]");
+    if (p->L < 32 || p->L > 1024 || (p->L & (p->L - 1)))
+        return set_error(LHC_EINVAL, "L must be a power of two in [32, 1024]");
+    const uint32_t kb = p->k_bloom ? p->k_bloom : p->k;
+    if (p->c == 0 || p->c % ((uint64_t)p->k * p->L)) return set_error(LHC_EINVAL, "c must be a positive multiple of k*L");
+    if (p->m == 0 || p->m % ((uint64_t)kb * p->L)) return set_error(LHC_EINVAL, "m must be a positive multiple of k_bloom*L");
+    if (p->c >= (1ull << 32)) return set_error(LHC_EINVAL, "c must be < 2^32");
+    if (p->m / p->L >= (1ull << 32)) return set_error(LHC_EINVAL, "m/L must be < 2^32");
+    return LHC_OK;
+}
+
+KParams kparams(const lhc_params* p) {
+    KParams K{};
+    K.seed = p->seed;
+    K.c = p->c;
+    K.m = p->m;
+    K.d = p->d;
+    K.k = p->k;
+    K.kb = p->k_bloom ? p->k_bloom : p->k;
+    K.L = p->L;
+    K.log2L = ilog2(p->L);
+    K.nw = p->L / 32;
+    K.log2nw = ilog2(K.nw);
+    K.S_Y = (uint32_t)(p->c / ((uint64_t)K.k * p->L));
+    K.S_B = (uint32_t)(p->m / ((uint64_t)K.kb * p->L));
+    K.nrows = (uint32_t)(((uint64_t)p->d + p->L - 1) / p->L);
+    return K;
+}
+
+WsLayout ws_layout(const KParams& P, uint64_t cap) {
+    WsLayout W{};
+    const uint64_t nrows = P.nrows;
+    W.ntiles = (uint32_t)(((uint64_t)P.d + kQueryTile - 1) / kQueryTile);
+    W.nchunks = (uint32_t)(((uint64_t)P.d + kTile - 1) / kTile);
+    size_t o = 0;
+    W.ctrl = o;      o = align_up(o + sizeof(Ctrl), 256);
+    W.tabS = o;      o = align_up(o + nrows * P.k * sizeof(uint2), 256);
+    W.tabB = o;      o = align_up(o + nrows * P.kb * sizeof(uint2), 256);
+    W.tile_cnt = o;  o = align_up(o + (W.ntiles + 1) * sizeof(uint32_t), 256);
+    W.chunk_off = o; o = align_up(o + (W.nchunks + 1) * sizeof(uint32_t), 256);
+    W.cells = o;     o = align_up(o + P.c * sizeof(CellState), 256);
+    W.claim = o;     o = align_up(o + std::max<uint64_t>(cap, 1) * sizeof(uint32_t), 256);
+    W.frontier = o;  o = align_up(o + P.c * sizeof(uint32_t), 256);
+    W.total = o;
+    return W;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace lhc
+
+using namespace lhc;
+
+extern "C" {
+
+int lhc_validate(const lhc_params* p) { return validate(p); }
+
+const char* lhc_last_error(void) { return g_err; }
+
+int lhc_last_launch_count(void) { return g_launches; }
+
+uint64_t lhc_bitmap_words(const lhc_params* p) { return validate(p) ? 0 : p->m / 32; }
+
+size_t lhc_decompress_workspace(const lhc_params* p, uint64_t cap_cand) {
+    if (validate(p)) return 0;
+    return ws_layout(kparams(p), cap_cand).total;
+}
+
+int sketch_hash_rows(const lhc_params* p, uint32_t dom, uint64_t n_rows, uint32_t* out,
+                     void* stream) {
+    reset_launches();
+    if (int rc = validate(p)) return rc;
+    if (dom > 1) return set_error(LHC_EINVAL, "dom must be 0 or 1");
+    if (!out && n_rows) return set_error(LHC_EINVAL, "out is NULL");
+    if (n_rows >= (1ull << 48)) return set_error(LHC_EINVAL, "n_rows must be < 2^48");
+    launch_hash_rows(kparams(p), dom, n_rows, reinterpret_cast<uint2*>(out), (cudaStream_t)stream);
+    return check_launch("sketch_hash_rows");
+}
+
+int sketch_clear(const lhc_params* p, uint32_t* bitmap, float* counters, void* stream) {
+    reset_launches();
+    if (int rc = validate(p)) return rc;
+    if (!bitmap || !counters) return set_error(LHC_EINVAL, "NULL sketch buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(bitmap, 0, p->m / 8, s) != cudaSuccess ||
+        cudaMemsetAsync(counters, 0, p->c * sizeof(float), s) != cudaSuccess)
+        return check_launch("sketch_clear");
+    return LHC_OK;
+}
+
+int sketch_compress(const lhc_params* p, const float* x, uint32_t* bitmap, float* counters,
+                    unsigned long long* nnz_out, void* stream) {
+    reset_launches();
+    if (int rc = validate(p)) return rc;
+    if (!x || !bitmap || !counters) return set_error(LHC_EINVAL, "NULL buffer");
+    if (!aligned16(x) || !aligned16(counters) || !aligned16(bitmap))
+        return set_error(LHC_EINVAL, "x, bitmap and counters must be 16-byte aligned");
+    launch_compress_dense(kparams(p), x, bitmap, counters, nnz_out, (cudaStream_t)stream);
+    return check_launch("sketch_compress");
+}
+
+int sketch_compress_coo(const lhc_params* p, uint64_t nnz, const uint32_t* idx,
+                        const float* val, uint32_t* bitmap, float* counters, void* stream) {
+    reset_launches();
+    if (int rc = validate(p)) return rc;
+    if (nnz && (!idx || !val)) return set_error(LHC_EINVAL, "NULL idx/val");
+    if (!bitmap || !counters) return set_error(LHC_EINVAL, "NULL sketch buffer");
+    if (nnz > p->d) return set_error(LHC_EINVAL, "nnz > d");
+    launch_compress_coo(kparams(p), nnz, idx, val, bitmap, counters, (cudaStream_t)stream);
+    return check_launch("sketch_compress_coo");
+}
+
+int sketch_aggregate(const lhc_params* p, int n_in, const uint32_t* const* bitmaps,
+                     const float* const* counters, uint32_t* out_bitmap, float* out_counters,
+                     void* stream) {
+    reset_launches();
+    if (int rc = validate(p)) return rc;
+    if (n_in < 1 || !bitmaps || !counters) return set_error(LHC_EINVAL, "need n_in >= 1 inputs");
+    if (!out_bitmap || !out_counters) return set_error(LHC_EINVAL, "NULL output");
+    for (int r = 0; r < n_in; r++)
+        if (!bitmaps[r] || !counters[r] || !aligned16(bitmaps[r]) || !aligned16(counters[r]))
+            return set_error(LHC_EINVAL, "input %d is NULL or not 16-byte aligned", r);
+    if (!aligned16(out_bitmap) || !aligned16(out_counters))
+        return set_error(LHC_EINVAL, "outputs must be 16-byte aligned");
+    launch_aggregate(p->m / 32, p->c, n_in, bitmaps, counters, out_bitmap, out_counters,
+                     (cudaStream_t)stream);
+    return check_launch("sketch_aggregate");
+}
+
+int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* counters,
+                      void* ws, size_t ws_bytes, uint64_t cap_cand, uint32_t* out_idx,
+                      float* out_val, uint8_t* out_peeled, float* out_dense, lhc_stats* stats,
+                      void* stream) {
+    reset_launches();
+    if (int rc = validate(p)) return rc;
+    if (!bitmap || !counters || !ws || !stats) return set_error(LHC_EINVAL, "NULL buffer");
+    if (cap_cand && (!out_idx || !out_val || !out_peeled)) return set_error(LHC_EINVAL, "NULL output");
+    if (cap_cand > p->d) cap_cand = p->d;
+    if (!aligned16(ws) || !aligned16(counters) || (out_dense && !aligned16(out_dense)))
+        return set_error(LHC_EINVAL, "ws, counters and out_dense must be 16-byte aligned");
+    const KParams P = kparams(p);
+    const WsLayout W = ws_layout(P, cap_cand);
+    if (ws_bytes < W.total)
+        return set_error(LHC_ECAPACITY, "workspace too small: %zu < %zu bytes", ws_bytes, W.total);
+    cudaStream_t s = (cudaStream_t)stream;
+    char* b = static_cast<char*>(ws);
+    Ctrl* ctrl = reinterpret_cast<Ctrl*>(b + W.ctrl);
+    uint2* tabS = reinterpret_cast<uint2*>(b + W.tabS);
+    uint2* tabB = reinterpret_cast<uint2*>(b + W.tabB);
+    uint32_t* tile_cnt = reinterpret_cast<uint32_t*>(b + W.tile_cnt);
+    uint32_t* chunk_off = reinterpret_cast<uint32_t*>(b + W.chunk_off);
+    CellState* cells = reinterpret_cast<CellState*>(b + W.cells);
+    uint32_t* claim = reinterpret_cast<uint32_t*>(b + W.claim);
+    uint32_t* frontier = reinterpret_cast<uint32_t*>(b + W.frontier);
+
+    if (cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), s) != cudaSuccess) return check_launch("memset");
+    if (cudaMemsetAsync(stats, 0, sizeof(lhc_stats), s) != cudaSuccess) return check_launch("memset");
+    launch_hash_rows(P, 0, P.nrows, tabS, s);
+    launch_hash_rows(P, 1, P.nrows, tabB, s);
+    launch_query_count(P, bitmap, tabB, tile_cnt, W.ntiles, s);
+    launch_query_scan(tile_cnt, W.ntiles, cap_cand, ctrl, stats, s);
+    launch_query_write(P, bitmap, tabB, tile_cnt, chunk_off, W.ntiles, cap_cand, out_idx, s);
+    if (int rc = check_launch("sketch_decompress/query")) return rc;
+    cudaError_t e = launch_peel(P, counters, tabS, out_idx, cap_cand, cells, claim, frontier, ctrl,
+                                out_val, out_peeled, stats, s);
+    if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
+    if (out_dense) launch_densify(P, bitmap, tabB, chunk_off, cap_cand, out_val, out_dense, s);
+    return check_launch("sketch_decompress");
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// launch.h — host-side launchers of the sm_100a kernels (internal to liblhc.so).
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lhc_internal.cuh"
+
+namespace lhc {
+
+int num_sms();           // SM count of the current device (cached per device)
+void count_launch(int n = 1);  // bench accounting (thread-local)
+void reset_launches();
+int set_error(int code, const char* fmt, ...);
+int validate(const lhc_params* p);
+KParams kparams(const lhc_params* p);
+
+void launch_hash_rows(const KParams& P, uint32_t dom, uint64_t n_rows, uint2* out, cudaStream_t s);
+void launch_compress_dense(const KParams& P, const float* x, uint32_t* bitmap, float* counters,
+                           unsigned long long* nnz_out, cudaStream_t s);
+void launch_compress_coo(const KParams& P, uint64_t nnz, const uint32_t* idx, const float* val,
+                         uint32_t* bitmap, float* counters, cudaStream_t s);
+void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* const* bitmaps,
+                      const float* const* counters, uint32_t* out_bitmap, float* out_counters,
+                      cudaStream_t s);
+// query + compaction + densify (query.cu)
+void launch_query_count(const KParams& P, const uint32_t* bitmap, const uint2* tabB,
+                        uint32_t* tile_cnt, uint32_t ntiles, cudaStream_t s);
+void launch_query_scan(uint32_t* tile_cnt, uint32_t ntiles, uint64_t cap, Ctrl* ctrl,
+                       lhc_stats* stats, cudaStream_t s);
+void launch_query_write(const KParams& P, const uint32_t* bitmap, const uint2* tabB,
+                        const uint32_t* tile_off, uint32_t* chunk_off, uint32_t ntiles,
+                        uint64_t cap, uint32_t* out_idx, cudaStream_t s);
+void launch_densify(const KParams& P, const uint32_t* bitmap, const uint2* tabB,
+                    const uint32_t* chunk_off, uint64_t cap, const float* out_val,
+                    float* out_dense, cudaStream_t s);
+// peeling decoder (peel.cu)
+cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
+                        const uint32_t* cand, uint64_t cap, CellState* cells, uint32_t* claim,
+                        uint32_t* frontier, Ctrl* ctrl, float* out_val, uint8_t* out_peeled,
+                        lhc_stats* stats, cudaStream_t s);
+
+WsLayout ws_layout(const KParams& P, uint64_t cap);
+
+}  // namespace lhc

@@ -1,0 +1,92 @@
+// lhc_internal.cuh — shared device helpers of the sm_100a kernels (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/lhc.h"
+
+namespace lhc {
+
+constexpr int kMaxK = 8;          // max Count Sketch hashes / Bloom probes
+constexpr uint32_t kTile = 1024;  // coordinates per compress tile / query chunk
+
+// Kernel-side view of lhc_params with the derived sizes precomputed on the host.
+struct KParams {
+    uint64_t seed;
+    uint64_t c;        // cells
+    uint64_t m;        // bits
+    uint32_t d;
+    uint32_t k;        // sketch hashes
+    uint32_t kb;       // bloom probes
+    uint32_t L;        // batch width
+    uint32_t log2L;
+    uint32_t nw;       // 32-bit words per row = L/32
+    uint32_t log2nw;
+    uint32_t S_Y;      // rows per sketch partition
+    uint32_t S_B;      // rows per bloom partition
+    uint32_t nrows;    // ceil(d / L)
+};
+
+// ---------------------------------------------------------------------------
+// Hash (reading R1, include/lhc.h header comment).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+__host__ __device__ __forceinline__ uint64_t hash_row(uint64_t seed, uint32_t dom, uint32_t j,
+                                                      uint64_t i) {
+    uint64_t key = ((uint64_t)dom << 56) | ((uint64_t)j << 48) | i;
+    return mix64(seed ^ mix64(key + 0x9E3779B97F4A7C15ull));
+}
+
+// Packed row map: x = absolute row (partition j), y = bias | (sign<0) << 31.
+__host__ __device__ __forceinline__ uint2 row_map(uint64_t seed, uint32_t dom, uint32_t j,
+                                                  uint64_t i, uint32_t S, uint32_t L) {
+    uint64_t H = hash_row(seed, dom, j, i);
+    uint32_t row = j * S + (uint32_t)(((H >> 32) * (uint64_t)S) >> 32);
+    uint32_t y = (uint32_t)(H & (uint64_t)(L - 1)) | ((uint32_t)((H >> 16) & 1u) << 31);
+    return make_uint2(row, y);
+}
+
+__device__ __forceinline__ uint32_t map_bias(uint2 mp) { return mp.y & 0x7fffffffu; }
+__device__ __forceinline__ float map_sign(uint2 mp) { return (mp.y >> 31) ? -1.0f : 1.0f; }
+
+// Decode state of one Count Sketch cell, 16 bytes so one sector serves both.
+//   key = sum over unpeeled candidates s in the cell of (2^32 + s): the degree is
+//         key >> 32 exactly whenever it is 0 or 1 (then the slot is (uint32)key),
+//         and >= 2 whenever the true degree is >= 2 (degree < 2^31 always holds
+//         since degree <= rows mapped to a cell < 2^27).
+//   R   = residual counter.
+struct __align__(16) CellState {
+    unsigned long long key;
+    float R;
+    uint32_t pad;
+};
+
+// Control block of one decompress call (workspace, zeroed per call).
+struct Ctrl {
+    unsigned long long n_cand;  // written by the query scan
+    uint32_t overflow;
+    uint32_t qtail;             // frontier queue tail
+    uint32_t n_peeled;
+    uint32_t rounds;
+    uint32_t pad[2];
+};
+
+// Sub-allocation of the decompress workspace.
+struct WsLayout {
+    size_t tabS, tabB, tile_cnt, chunk_off, cells, claim, frontier, ctrl, total;
+    uint32_t ntiles, nchunks;
+};
+
+constexpr uint32_t kQueryTile = 32 * kTile;  // coordinates per query CTA tile (32 chunks)
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace lhc

@@ -1,0 +1,126 @@
+"""Host-side sizing of the sketch S(X) = [Y, B] (no device work).
+
+The workers must agree on (m, c) before any gradient is seen (reading R15), so
+both are derived from the expected aggregate support:
+
+* expected union support of W workers with independent supports of density rho
+  (reading R19): ``n = d * (1 - (1 - rho)^W)``;
+* Bloom false-positive rate of a partitioned filter with k_B probes over m bits
+  (one partition of m/k_B bits per probe):
+  ``eps(m) = (1 - (1 - k_B/m)^n)^k_B``;
+* candidates ``n_c = n + eps * (d - n)`` (the table records
+  ``eps (N - n)`` redundant values);
+* Count Sketch cells ``c = gamma_s * n_c`` rounded up to a multiple of k*L, with
+  the provisioning gamma_s >= gamma = 1.23 (reading R14: 1.30 default);
+* m minimises the sketch bits ``m + 32 c`` over multiples of k_B*L.
+
+Also the §3.3 theory helpers: S_min, the optimal eps and the
+(S1, S2) sizes of the paper's Bloom + Count Sketch construction.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+GAMMA_PAPER = 1.23
+GAMMA_DEFAULT = 1.30      # reading R14
+GAMMA_STAR_K3 = 1.0 / 0.8184691  # exact 2-core threshold of random 3-hypergraphs
+
+
+def union_support(d: int, density: float, workers: int) -> float:
+    return d * (1.0 - (1.0 - density) ** workers)
+
+
+def bloom_fp_rate(m: int, n: float, k_bloom: int) -> float:
+    """False-positive rate of a k_bloom-partitioned Bloom filter of m bits, n items."""
+    if m <= 0:
+        return 1.0
+    return (1.0 - (1.0 - k_bloom / m) ** n) ** k_bloom
+
+
+@dataclass
+class Sizing:
+    d: int
+    m: int
+    c: int
+    k: int
+    k_bloom: int
+    L: int
+    n_expected: float
+    eps: float
+    n_cand_expected: float
+    gamma: float
+
+    @property
+    def sketch_bytes(self) -> int:
+        return self.m // 8 + 4 * self.c
+
+    @property
+    def ratio(self) -> float:
+        """Sketch size / dense fp32 size."""
+        return self.sketch_bytes / (4.0 * self.d)
+
+
+def _round_up(x: float, q: int) -> int:
+    return int(math.ceil(x / q)) * q
+
+
+def size_for(d: int, n: float, k: int = 3, k_bloom: int = 0, L: int = 1024,
+             gamma: float = GAMMA_DEFAULT) -> Sizing:
+    """(m, c) minimising m + 32c for an expected aggregate support of n coordinates."""
+    kb = k_bloom or k
+    qm, qc = kb * L, k * L
+    n = max(float(n), 1.0)
+    best = None
+    # scan bits per expected item from 1 to 64 (fine grid), then refine locally
+    grid = [0.25 * i for i in range(4, 257)]
+    for bpe in grid:
+        m = max(qm, _round_up(bpe * n, qm))
+        eps = bloom_fp_rate(m, n, kb)
+        nc = n + eps * (d - n)
+        c = max(qc, _round_up(gamma * nc, qc))
+        cost = m + 32 * c
+        if best is None or cost < best[0]:
+            best = (cost, m, c, eps, nc)
+    _, m, c, eps, nc = best
+    return Sizing(d, m, c, k, kb, L, n, eps, nc, gamma)
+
+
+def size_workload(d: int, density: float, workers: int, **kw) -> Sizing:
+    return size_for(d, union_support(d, density, workers), **kw)
+
+
+# ---- §3.3 theory ------------------------------------------------
+
+def binary_entropy(x: float) -> float:
+    if x <= 0.0 or x >= 1.0:
+        return 0.0
+    return -x * math.log2(x) - (1 - x) * math.log2(1 - x)
+
+
+def f0(x: float) -> float:
+    """f(0, x) = (x + 1) H(1 / (x + 1))."""
+    return (x + 1.0) * binary_entropy(1.0 / (x + 1.0))
+
+
+def s_min_bits(n: float, lam: float, C: int) -> float:
+    """S_min = n f(0, lambda) + n log2(2^C - 1)."""
+    return n * f0(lam) + n * math.log2(2.0 ** C - 1.0)
+
+
+def optimal_eps(C: int, lam: float, gamma: float = GAMMA_PAPER) -> float:
+    """eps = (ln^2 2 * gamma * C * lambda)^-1, clamped to 1."""
+    return min(1.0, 1.0 / (math.log(2) ** 2 * gamma * C * lam))
+
+
+def bloom_bits(n: float, eps: float) -> float:
+    """n / ln 2 * log2(1/eps)."""
+    return n / math.log(2) * math.log2(1.0 / eps)
+
+
+def paper_sizes(n: float, lam: float, C: int, gamma: float = GAMMA_PAPER):
+    """(S1, S2) of P:L244-247 at the optimal eps."""
+    eps = optimal_eps(C, lam, gamma)
+    s1 = bloom_bits(n, eps)
+    s2 = gamma * C * n * (1.0 + eps * lam)
+    return s1, s2

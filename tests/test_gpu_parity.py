@@ -1,0 +1,328 @@
+"""GPU parity: every step of the sm_100a path, through the C ABI, against the CPU
+oracle on the same seeded inputs (-m gpu).
+
+Bars (north star): bitmaps, candidate lists, peel flags, success and rounds
+bit-exact; fp32 values within 1e-5 relative + 1e-7 absolute of the fp64 oracle
+(|gpu - ora| <= 1e-7 + 1e-5 |ora|); under the dyadic law every fp32 sum is exact,
+so values must be bit-identical too.
+"""
+import numpy as np
+import pytest
+
+from lhc_inputs import config, rng_for, support, values
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-7
+
+
+@pytest.fixture(scope="module")
+def lhc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2402_07529_b200 as lhc
+
+    lhc.lib()
+    return lhc
+
+
+def U(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def F(t):
+    return t.cpu().numpy().astype(np.float64)
+
+
+def gpu_params(lhc, d, m, c, k=3, kb=0, L=1024, seed=0):
+    return lhc.params(d, m, c, k, kb, L, seed)
+
+
+def ora_params(ora, p):
+    return ora.params(p.d, p.m, p.c, p.k, p.k_bloom, p.L, p.seed)
+
+
+def make_workers(d, nnz, W, seed, law="dyadic", structure="uniform", run=64, sigma=1e-3):
+    xs = []
+    for w in range(W):
+        rng = rng_for(seed + w)
+        idx = support(rng, d, nnz, structure, run)
+        x = np.zeros(d, np.float32)
+        x[idx] = values(rng, len(idx), law, sigma)
+        xs.append(x)
+    return xs
+
+
+def assert_values(gpu, ref, exact):
+    if exact:
+        assert np.array_equal(gpu, ref)
+    else:
+        err = np.abs(gpu - ref)
+        bad = err > ATOL + RTOL * np.abs(ref)
+        assert not bad.any(), (int(bad.sum()), float(err.max()))
+
+
+# ---------------------------------------------------------------- hash kernel --
+
+@pytest.mark.parametrize("L", [32, 128, 1024])
+def test_hash_rows_bit_exact(lhc, ora, L):
+    p = gpu_params(lhc, 5_000_000, 3 * L * 1117, 3 * L * 733, L=L, seed=0xDEADBEEF12345)
+    op = ora_params(ora, p)
+    n = 3000
+    for dom in (0, 1):
+        out = torch.empty(2 * n * 3, dtype=torch.int32, device="cuda")
+        lhc.sketch_hash_rows(p, dom, n, out)
+        got = U(out).reshape(n, 3, 2)
+        for i in range(0, n, 7):
+            for j in range(3):
+                row, bias, sign = ora.row_map(op, dom, j, i)
+                assert got[i, j, 0] == row
+                assert got[i, j, 1] == (bias | ((1 << 31) if sign < 0 else 0))
+
+
+# ------------------------------------------------------------------ compress --
+
+CASES = [
+    # d, nnz per worker, W, L, structure
+    (10_000, 100, 2, 1024, "uniform"),          # tiny config
+    (1_000_003, 10_000, 3, 1024, "uniform"),    # many tiles + ragged tail
+    (1_000_003, 10_000, 2, 32, "uniform"),      # smallest batch width
+    (777_777, 30_000, 4, 256, "runs"),          # runs, L=256
+    (4099, 4099, 1, 64, "uniform"),             # fully dense, tail < 4
+]
+
+
+@pytest.mark.parametrize("d,nnz,W,L,structure", CASES)
+@pytest.mark.parametrize("law", ["dyadic", "gauss"])
+def test_compress_dense(lhc, ora, d, nnz, W, L, structure, law):
+    s = lhc.size_workload(d, nnz / d, W, L=L)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=77 + L)
+    op = ora_params(ora, p)
+    xs = make_workers(d, nnz, W, 1000 + d % 97, law, structure)
+    sk = lhc.Sketch(p)
+    sk.clear()
+    nnz_out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for x in xs:
+        sk.compress(torch.from_numpy(x).cuda(), nnz_out)
+    B, Y = None, None
+    for x in xs:
+        B, Y = ora.compress_dense(op, x, B, Y)
+    assert np.array_equal(U(sk.bitmap), B)
+    assert_values(F(sk.counters), Y, exact=(law == "dyadic"))
+    assert int(nnz_out.item()) == sum(int((x != 0).sum()) for x in xs)
+
+
+def test_compress_coo(lhc, ora):
+    d, L = 900_001, 512
+    s = lhc.size_workload(d, 0.02, 1, L=L)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=5)
+    rng = rng_for(42)
+    idx = support(rng, d, 18_000, "runs", 64)
+    val = values(rng, len(idx), "dyadic")
+    val[::97] = 0.0  # listed zeros are still inserted
+    sk = lhc.Sketch(p)
+    sk.clear()
+    sk.compress_coo(torch.from_numpy(idx.view(np.int32)).cuda(), torch.from_numpy(val).cuda())
+    B, Y = ora.compress_coo(ora_params(ora, p), idx, val)
+    assert np.array_equal(U(sk.bitmap), B)
+    assert np.array_equal(F(sk.counters), Y)
+
+
+def test_aggregate(lhc, ora):
+    d, L, W = 500_000, 1024, 5
+    s = lhc.size_workload(d, 0.01, W)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=9)
+    op = ora_params(ora, p)
+    xs = make_workers(d, 5000, W, 77)
+    sks = []
+    for x in xs:
+        sk = lhc.Sketch(p)
+        sk.clear()
+        sk.compress(torch.from_numpy(x).cuda())
+        sks.append(sk)
+    out = lhc.Sketch(p)
+    lhc.aggregate(p, sks, out)
+    ref = [ora.compress_dense(op, x) for x in xs]
+    B, Y = ora.aggregate([r[0] for r in ref], [r[1] for r in ref])
+    assert np.array_equal(U(out.bitmap), B)
+    assert np.array_equal(F(out.counters), Y)
+    # in place (out aliases input 0)
+    lhc.aggregate(p, sks, sks[0])
+    assert np.array_equal(U(sks[0].bitmap), B)
+
+
+# ---------------------------------------------------------------- decompress --
+
+def run_decode(lhc, p, B, Y, cap=None, dense=True):
+    """Decode oracle-independent sketch bytes B (u32) / Y (fp32) on the GPU."""
+    sk = lhc.Sketch(p)
+    sk.bitmap.copy_(torch.from_numpy(B.view(np.int32)))
+    sk.counters.copy_(torch.from_numpy(Y.astype(np.float32)))
+    dec = lhc.Decoder(p, cap if cap is not None else p.d, dense=dense)
+    dec(sk)
+    torch.cuda.synchronize()
+    return dec
+
+
+def compare_decode(ora, dec, ref, exact):
+    st = dec.read_stats()
+    assert st["n_cand"] == ref.stats.n_cand
+    assert st["overflow"] == ref.stats.overflow
+    if ref.stats.overflow:
+        assert not st["success"]
+        return st
+    n = st["n_cand"]
+    assert np.array_equal(U(dec.idx[:n]), ref.cand)
+    assert np.array_equal(dec.peeled[:n].cpu().numpy().astype(bool), ref.peeled)
+    assert st["n_peeled"] == ref.stats.n_peeled
+    assert st["rounds"] == ref.stats.rounds
+    assert st["success"] == ref.stats.success
+    assert_values(F(dec.val[:n]), ref.val, exact)
+    if dec.dense is not None and ref.dense is not None:
+        dense = F(dec.dense)
+        assert_values(dense, ref.dense, exact)
+        cand = np.zeros(len(dense), bool)
+        cand[ref.cand] = True
+        assert not dense[~cand].any()  # exact zeros off the candidate set
+    return st
+
+
+@pytest.mark.parametrize("d,nnz,W,L,structure", CASES)
+@pytest.mark.parametrize("law", ["dyadic", "gauss"])
+def test_pipeline(lhc, ora, d, nnz, W, L, structure, law):
+    s = lhc.size_workload(d, nnz / d, W, L=L)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=0x5EED + d)
+    op = ora_params(ora, p)
+    xs = make_workers(d, nnz, W, 31 + d % 13, law, structure)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(op, xs)
+    assert np.array_equal(U(run.sketch.bitmap), B)
+    assert_values(F(run.sketch.counters), Y, law == "dyadic")
+    st = compare_decode(ora, dec, ref, law == "dyadic")
+    if law == "dyadic" and st["success"]:
+        assert np.array_equal(F(dec.dense), np.sum(np.stack(xs).astype(np.float64), axis=0))
+
+
+@pytest.mark.parametrize("gamma", [0.9, 1.1, 1.2, 1.25, 1.5])
+def test_decode_threshold_sweep(lhc, ora, gamma):
+    # near and below the peeling threshold: flags, rounds and the median fallback
+    d, L, n = 2_000_000, 1024, 40_000
+    rng = rng_for(int(gamma * 100))
+    idx = support(rng, d, n)
+    x = np.zeros(d, np.float32)
+    x[idx] = values(rng, n, "dyadic")
+    m = 3 * L * ((12 * n) // (3 * L))
+    c = 3 * L * max(1, int(round(gamma * n / (3 * L))))
+    p = gpu_params(lhc, d, m, c, L=L, seed=int(gamma * 1000))
+    op = ora_params(ora, p)
+    B, Y = ora.compress_dense(op, x)
+    ref = ora.decompress(op, B, Y)
+    dec = run_decode(lhc, p, B, Y)
+    # the GPU decodes fp32 counters; dyadic sums are exact so Y is the same bytes
+    compare_decode(ora, dec, ref, exact=True)
+
+
+def test_overflow_and_caps(lhc, ora):
+    d, L = 300_000, 1024
+    p = gpu_params(lhc, d, 3 * L * 8, 3 * L * 16, L=L, seed=3)
+    op = ora_params(ora, p)
+    x = np.zeros(d, np.float32)
+    x[::40] = 0.5
+    B, Y = ora.compress_dense(op, x)
+    n_c = len(ora.query(op, B))
+    for cap in (10, n_c - 1, n_c, n_c + 5):
+        ref = ora.decompress(op, B, Y, cap=cap)
+        dec = run_decode(lhc, p, B, Y, cap=cap)
+        compare_decode(ora, dec, ref, exact=True)
+
+
+def test_empty_and_degenerate(lhc, ora):
+    L = 1024
+    p = gpu_params(lhc, 5000, 3 * L, 3 * L, L=L, seed=1)
+    op = ora_params(ora, p)
+    B = np.zeros(p.words, np.uint32)
+    Y = np.zeros(p.c, np.float64)
+    dec = run_decode(lhc, p, B, Y)
+    st = dec.read_stats()
+    assert st["n_cand"] == 0 and st["success"] and st["rounds"] == 0
+    assert not F(dec.dense).any()
+    # d = 1
+    p1 = gpu_params(lhc, 1, 3 * 32, 3 * 32, L=32, seed=2)
+    x = np.array([0.25], np.float32)
+    B, Y, ref = ora.pipeline(ora_params(ora, p1), [x])
+    run = lhc.LosslessAllReduce(p1, cap_cand=1)
+    dec = run.step([torch.from_numpy(x).cuda()])
+    torch.cuda.synchronize()
+    compare_decode(ora, dec, ref, exact=True)
+    assert F(dec.dense).tolist() == [0.25]
+
+
+def test_determinism_of_indices_and_flags(lhc):
+    d, L = 2_000_000, 1024
+    s = lhc.size_workload(d, 0.01, 4)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=11)
+    xs = [torch.from_numpy(x).cuda() for x in make_workers(d, 20_000, 4, 8, "gauss")]
+    outs = []
+    for _ in range(2):
+        run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=4)
+        dec = run.step(xs)
+        torch.cuda.synchronize()
+        st = dec.read_stats()
+        n = st["n_cand"]
+        outs.append((U(run.sketch.bitmap).copy(), U(dec.idx[:n]).copy(),
+                     dec.peeled[:n].cpu().numpy().copy(), st["rounds"]))
+    assert all(np.array_equal(a, b) for a, b in zip(outs[0][:3], outs[1][:3]))
+    assert outs[0][3] == outs[1][3]
+
+
+# ------------------------------------------------- BASELINE.json full sizes --
+
+FULL = [
+    ("ncf", {}),
+    ("lstm", {}),
+    ("bert", {"density": 0.01}),
+    ("bert", {"density": 0.10}),
+    ("vgg", {}),
+]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,over", FULL, ids=[f"{n}-{o.get('density', '')}" for n, o in FULL])
+def test_full_size_configs(lhc, ora, name, over):
+    """The bench's launch configuration (per-worker sketches aggregated on one GPU,
+    one decode) at the configs' full sizes, compared in full with the oracle."""
+    wl = config(name, **over)
+    s = lhc.size_workload(wl.d, wl.density, wl.workers)
+    p = gpu_params(lhc, wl.d, s.m, s.c, seed=0x1DC0DE)
+    op = ora_params(ora, p)
+    xs = [wl.dense(w) for w in range(wl.workers)]
+    run = lhc.LosslessAllReduce(p, cap_cand=int(s.n_cand_expected * 1.5) + 1024,
+                                local_workers=wl.workers)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(op, xs)
+    assert np.array_equal(U(run.sketch.bitmap), B)
+    assert_values(F(run.sketch.counters), Y, exact=False)
+    st = compare_decode(ora, dec, ref, exact=False)
+    assert st["success"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("gamma", [1.10, 1.20, 1.22, 1.25, 1.30, 1.50])
+def test_vgg_gamma_sweep(lhc, ora, gamma):
+    """VGG19-shaped sketch-size sweep near the peeling threshold (dyadic values:
+    bit-exact everything, including the fallback estimates)."""
+    wl = config("vgg", law="dyadic")
+    s = lhc.size_workload(wl.d, wl.density, wl.workers, gamma=gamma)
+    p = gpu_params(lhc, wl.d, s.m, s.c, seed=0x1DC0DE)
+    op = ora_params(ora, p)
+    xs = [wl.dense(w) for w in range(wl.workers)]
+    run = lhc.LosslessAllReduce(p, cap_cand=int(s.n_cand_expected * 1.5), local_workers=wl.workers)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(op, xs, dense=False)
+    assert np.array_equal(U(run.sketch.bitmap), B)
+    compare_decode(ora, dec, ref, exact=True)

@@ -138,6 +138,7 @@ def run_reference(args, wl, rank):
     frac = 1.0
     cal = sample_workload(wl, 1 / 64)
     t_cal = oracle_step(oracle, cal, size_workload, args.gamma)
+    trace(f"oracle calibration: {t_cal:.3f} s on d={cal.d}")
     est_full = t_cal * 64
     if est_full > target:
         frac = max(1 / 64, target / est_full)
@@ -145,6 +146,7 @@ def run_reference(args, wl, rank):
     times = []
     for s in range(args.warmup + args.steps):
         t = oracle_step(oracle, sub, size_workload, args.gamma)
+        trace(f"oracle step {s}: {t:.2f} s on d={sub.d}")
         if s >= args.warmup:
             times.append(t)
     T = sum(times) / len(times)
@@ -183,8 +185,17 @@ def oracle_step(oracle, wl, size_workload, gamma):
 
 # ------------------------------------------------------------------- our arm --
 
+def trace(msg):
+    if os.environ.get("LHC_BENCH_TRACE"):
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
     args = parse()
+    if os.environ.get("LHC_BENCH_TRACE"):
+        import faulthandler
+
+        faulthandler.dump_traceback_later(int(os.environ.get("LHC_BENCH_TRACE")), exit=True)
     wl = workload(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -214,6 +225,7 @@ def main():
     cap = min(wl.d, int(sz.n_cand_expected * 1.25) + 4096)
     my_workers = [w for w in range(wl.workers) if w % world == rank]
 
+    trace('inputs')
     # inputs resident in HBM (generated on the host with the shared seeded recipe)
     host = [wl.dense(w) for w in my_workers]
     xs = [torch.from_numpy(x).to(dev) for x in host]
@@ -289,11 +301,13 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    trace('warmup')
     n_warm = max(3, args.warmup)  # timing rule: at least 3 untimed warm-up steps
     for _ in range(n_warm):
         step()
     barrier()
 
+    trace('timed')
     # ---- timed region: K steps, per-step events, L2 flushed between steps ----
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -333,6 +347,7 @@ def main():
 
     stats = run.decoder.read_stats()
 
+    trace('e2e')
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -369,6 +384,7 @@ def main():
         if not np.isfinite(e2e["value"]):
             e2e = None
 
+    trace('roofline')
     # ---- roofline of the dominant kernel (compress) ----
     import json as _json
 
@@ -386,9 +402,10 @@ def main():
                 "bytes_per_launch": bytes_compress, "avg_launch_us": avg_compress_ms * 1e3,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
 
+    trace('cpu baseline')
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ref = run_reference(argparse.Namespace(steps=1, warmup=0, gamma=args.gamma), wl, 0)
+        ref = run_reference(argparse.Namespace(steps=1, warmup=0, gamma=args.gamma, gpus=1), wl, 0)
         cpu = ref["cpu_baseline"] if ref else None
 
     if rank == 0:

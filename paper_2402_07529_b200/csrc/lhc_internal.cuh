@@ -73,10 +73,14 @@ struct __align__(16) CellState {
 struct Ctrl {
     unsigned long long n_cand;  // written by the query scan
     uint32_t overflow;
-    uint32_t qtail;             // frontier queue tail
-    uint32_t n_peeled;
-    uint32_t rounds;
-    uint32_t pad[2];
+    // Per-round counters, triple-buffered by round index r % 3: round r appends
+    // its new frontier cells after the current segment through qcnt[r % 3] and
+    // counts its peels in pcnt[r % 3]; both are read by every block after the
+    // grid barrier that ends round r (when they are final) and reset by block 0
+    // during round r + 2, when no block reads or writes them any more.
+    uint32_t qcnt[3];
+    uint32_t pcnt[3];
+    uint32_t pad;
 };
 
 // Sub-allocation of the decompress workspace.

@@ -46,12 +46,13 @@ __device__ __forceinline__ unsigned long long ld_key(const CellState* c) {
 }
 __device__ __forceinline__ float ld_R(const CellState* c) { return __ldcg(&c->R); }
 
-// Block-aggregated append of the (up to kMaxK per thread) cells in sh_q.
+// Block-aggregated append of the (up to kMaxK per thread) cells in sh_q to the
+// queue segment that starts at seg_base, through the round's counter qcnt.
 __device__ __forceinline__ void flush_queue(uint32_t* sh_q, uint32_t* sh_n, uint32_t* sh_base,
-                                            uint32_t* frontier, Ctrl* ctrl) {
+                                            uint32_t* frontier, uint32_t seg_base, uint32_t* qcnt) {
     __syncthreads();
     const uint32_t n = *sh_n;
-    if (threadIdx.x == 0 && n) *sh_base = atomicAdd(&ctrl->qtail, n);
+    if (threadIdx.x == 0 && n) *sh_base = seg_base + atomicAdd(qcnt, n);
     __syncthreads();
     for (uint32_t a = threadIdx.x; a < n; a += blockDim.x) frontier[*sh_base + a] = sh_q[a];
     __syncthreads();
@@ -103,18 +104,24 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     }
     grid.sync();
 
-    // F0: cells of degree one
+    // F0 ("round 0"): cells of degree one, appended through qcnt[0]
     for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < P.c; base += gstride) {
         const uint64_t e = base + threadIdx.x;
         if (e < P.c && (ld_key(cells + e) >> 32) == 1ull) sh_q[atomicAdd(&sh_n, 1u)] = (uint32_t)e;
-        flush_queue(sh_q, &sh_n, &sh_base, frontier, ctrl);
+        flush_queue(sh_q, &sh_n, &sh_base, frontier, 0u, &ctrl->qcnt[0]);
     }
     grid.sync();
 
     uint32_t f_begin = 0;
-    uint32_t f_end = *(volatile uint32_t*)&ctrl->qtail;
-    uint32_t peeled_before = 0, rounds = 0;
-    while (f_begin < f_end) {
+    uint32_t f_end = *(volatile uint32_t*)&ctrl->qcnt[0];
+    uint32_t n_peeled = 0, rounds = 0;
+    for (uint32_t r = 1; f_begin < f_end; r++) {
+        uint32_t* qcnt = &ctrl->qcnt[r % 3];
+        uint32_t* pcnt = &ctrl->pcnt[r % 3];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // counters of round r + 1 (last used r - 2)
+            ctrl->qcnt[(r + 1) % 3] = 0;
+            ctrl->pcnt[(r + 1) % 3] = 0;
+        }
         for (uint64_t base = f_begin + blockIdx.x * (uint64_t)blockDim.x; base < f_end;
              base += gstride) {
             const uint64_t f = base + threadIdx.x;
@@ -144,18 +151,18 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                     }
                 }
             }
-            flush_queue(sh_q, &sh_n, &sh_base, frontier, ctrl);
+            flush_queue(sh_q, &sh_n, &sh_base, frontier, f_end, qcnt);
         }
         if (threadIdx.x == 0 && sh_peeled) {
-            atomicAdd(&ctrl->n_peeled, sh_peeled);
+            atomicAdd(pcnt, sh_peeled);
             sh_peeled = 0;
         }
         grid.sync();
+        const uint32_t np = *(volatile uint32_t*)pcnt;
         f_begin = f_end;
-        f_end = *(volatile uint32_t*)&ctrl->qtail;
-        const uint32_t np = *(volatile uint32_t*)&ctrl->n_peeled;
-        if (np != peeled_before) rounds++;
-        peeled_before = np;
+        f_end += *(volatile uint32_t*)qcnt;
+        n_peeled += np;
+        if (np) rounds++;
     }
 
     // finalize: median estimate of unpeeled candidates
@@ -180,9 +187,9 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        stats->n_peeled = peeled_before;
+        stats->n_peeled = n_peeled;
         stats->rounds = rounds;
-        stats->success = (uint64_t)peeled_before == n_c ? 1 : 0;
+        stats->success = (uint64_t)n_peeled == n_c ? 1 : 0;
     }
 }
 

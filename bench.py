@@ -223,7 +223,7 @@ def main():
     sz = lhc.size_workload(wl.d, wl.density, wl.workers, gamma=args.gamma)
     p = lhc.params(wl.d, sz.m, sz.c, 3, 0, 1024, SEED)
     cap = min(wl.d, int(sz.n_cand_expected * 1.25) + 4096)
-    my_workers = [w for w in range(wl.workers) if w % world == rank]
+    my_workers = lhc.pipeline.owned_workers(wl.workers, rank, world)
 
     trace('inputs')
     # inputs resident in HBM (generated on the host with the shared seeded recipe)

@@ -83,17 +83,18 @@ KParams kparams(const lhc_params* p) {
 WsLayout ws_layout(const KParams& P, uint64_t cap) {
     WsLayout W{};
     const uint64_t nrows = P.nrows;
-    W.ntiles = (uint32_t)(((uint64_t)P.d + kQueryTile - 1) / kQueryTile);
     W.nchunks = (uint32_t)(((uint64_t)P.d + kTile - 1) / kTile);
     size_t o = 0;
     W.ctrl = o;      o = align_up(o + sizeof(Ctrl), 256);
     W.tabS = o;      o = align_up(o + nrows * P.k * sizeof(uint2), 256);
-    W.tabB = o;      o = align_up(o + nrows * P.kb * sizeof(uint2), 256);
-    W.tile_cnt = o;  o = align_up(o + (W.ntiles + 1) * sizeof(uint32_t), 256);
-    W.chunk_off = o; o = align_up(o + (W.nchunks + 1) * sizeof(uint32_t), 256);
+    W.gmask = o;     o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);
+    W.chunk_cnt = o; o = align_up(o + (size_t)W.nchunks * sizeof(uint32_t), 256);
+    W.chunk_off = o; o = align_up(o + (size_t)W.nchunks * sizeof(uint32_t), 256);
+    W.cta_total = o; o = align_up(o + kMaxQueryCtas * sizeof(uint32_t), 256);
     W.cells = o;     o = align_up(o + P.c * sizeof(CellState), 256);
     W.claim = o;     o = align_up(o + std::max<uint64_t>(cap, 1) * sizeof(uint32_t), 256);
-    W.frontier = o;  o = align_up(o + P.c * sizeof(uint32_t), 256);
+    W.ccell = o;     o = align_up(o + peel_ccell_bytes(P.k, cap), 256);
+    W.frontier = o;  o = align_up(o + P.c * sizeof(uint2), 256);
     W.total = o;
     return W;
 }
@@ -199,25 +200,25 @@ int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* 
     char* b = static_cast<char*>(ws);
     Ctrl* ctrl = reinterpret_cast<Ctrl*>(b + W.ctrl);
     uint2* tabS = reinterpret_cast<uint2*>(b + W.tabS);
-    uint2* tabB = reinterpret_cast<uint2*>(b + W.tabB);
-    uint32_t* tile_cnt = reinterpret_cast<uint32_t*>(b + W.tile_cnt);
+    uint32_t* gmask = reinterpret_cast<uint32_t*>(b + W.gmask);
+    uint32_t* chunk_cnt = reinterpret_cast<uint32_t*>(b + W.chunk_cnt);
     uint32_t* chunk_off = reinterpret_cast<uint32_t*>(b + W.chunk_off);
+    uint32_t* cta_total = reinterpret_cast<uint32_t*>(b + W.cta_total);
     CellState* cells = reinterpret_cast<CellState*>(b + W.cells);
     uint32_t* claim = reinterpret_cast<uint32_t*>(b + W.claim);
-    uint32_t* frontier = reinterpret_cast<uint32_t*>(b + W.frontier);
+    uint32_t* ccell = reinterpret_cast<uint32_t*>(b + W.ccell);
+    uint2* frontier = reinterpret_cast<uint2*>(b + W.frontier);
 
+    if (query_max_ctas() > kMaxQueryCtas) return set_error(LHC_ECUDA, "device too large for the query grid");
     if (cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), s) != cudaSuccess) return check_launch("memset");
     if (cudaMemsetAsync(stats, 0, sizeof(lhc_stats), s) != cudaSuccess) return check_launch("memset");
-    launch_hash_rows(P, 0, P.nrows, tabS, s);
-    launch_hash_rows(P, 1, P.nrows, tabB, s);
-    launch_query_count(P, bitmap, tabB, tile_cnt, W.ntiles, s);
-    launch_query_scan(tile_cnt, W.ntiles, cap_cand, ctrl, stats, s);
-    launch_query_write(P, bitmap, tabB, tile_cnt, chunk_off, W.ntiles, cap_cand, out_idx, s);
-    if (int rc = check_launch("sketch_decompress/query")) return rc;
-    cudaError_t e = launch_peel(P, counters, tabS, out_idx, cap_cand, cells, claim, frontier, ctrl,
-                                out_val, out_peeled, stats, s);
+    cudaError_t e = launch_query(P, bitmap, tabS, gmask, chunk_cnt, chunk_off, cta_total, cap_cand,
+                                 out_idx, ctrl, stats, s);
+    if (e != cudaSuccess) return set_error(LHC_ECUDA, "query launch: %s", cudaGetErrorString(e));
+    e = launch_peel(P, counters, tabS, out_idx, cap_cand, cells, claim, ccell, frontier, ctrl,
+                    out_val, out_peeled, stats, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
-    if (out_dense) launch_densify(P, bitmap, tabB, chunk_off, cap_cand, out_val, out_dense, s);
+    if (out_dense) launch_densify(P, gmask, chunk_off, cap_cand, out_val, out_dense, s);
     return check_launch("sketch_decompress");
 }
 

@@ -33,119 +33,139 @@ void launch_hash_rows(const KParams& P, uint32_t dom, uint64_t n_rows, uint2* ou
 // ---------------------------------------------------------------------------
 // Dense compression.
 //
-// One CTA of 256 threads processes a tile of 1024 consecutive coordinates per
-// iteration (one 128-bit load per thread, next tile prefetched into registers);
-// a tile holds 1024/L input rows.  Per tile:
-//   1. threads < rows*(k+kb) compute the tile's row maps into shared memory
-//      (one hash per input row and probe, "each batch shares the same
-//      index");
-//   2. the nonzero mask of the tile is built as 32 words with 8-lane OR
-//      reductions of per-thread nibbles;
-//   3. Bloom filter: thread (j, w) assembles destination word w of probe j's
-//      row by a funnel shift of two source words (the rotation by bias_j, so a
-//      row maps to exactly one row of B) and issues one atomicOr per nonzero
-//      word — at most k_bloom*L/32 atomics per input row instead of one per bit;
-//   4. Count Sketch: each nonzero adds sign_j * x to its k cells with a
-//      fire-and-forget fp32 reduction (RED.ADD.F32 at L2).
+// One warp owns a chunk of 1024 consecutive coordinates at a time (1024/L input
+// rows) and needs no block-level synchronisation:
+//   1. eight 128-bit streaming loads per lane (the whole 4 KB chunk in flight);
+//   2. lanes compute the chunk's row maps (one hash per input row and probe,
+//      P:L261 "each batch shares the same index") into a warp-private slice of
+//      shared memory;
+//   3. the chunk's nonzero mask is assembled as 32 words, lane w holding word w
+//      (8-lane OR reductions of per-lane nibbles);
+//   4. Bloom filter: for probe j, lane w builds destination word w of its row's
+//      destination row (the rotation by bias_j is two shuffles and a funnel
+//      shift, so a row maps onto exactly one row of B) and issues one atomicOr
+//      if it is nonzero — at most k_bloom*L/32 atomics per input row;
+//   5. Count Sketch: each nonzero adds sign_j * x to its k cells with a
+//      fire-and-forget fp32 reduction (RED.ADD.F32, performed at L2).
 // ---------------------------------------------------------------------------
 constexpr int kCompressThreads = 256;
-
-__device__ __forceinline__ float4 load_tile4(const float* __restrict__ x, uint64_t q, uint32_t d) {
-    if (q + 3 < d) return __ldcs(reinterpret_cast<const float4*>(x + q));
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (q < d) v.x = x[q];
-    if (q + 1 < d) v.y = x[q + 1];
-    if (q + 2 < d) v.z = x[q + 2];
-    return v;
-}
+constexpr int kCompressWarps = kCompressThreads / 32;
+constexpr uint32_t kFullMask = 0xffffffffu;
 
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ bitmap,
                  float* __restrict__ counters, unsigned long long* __restrict__ nnz_out) {
-    __shared__ uint2 sh_map[32 * 2 * kMaxK];
-    __shared__ uint32_t sh_src[32];
-    __shared__ unsigned long long sh_nnz;
-
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t ntiles = (uint32_t)((P.d + kTile - 1) / kTile);
-    const uint32_t rpt_log2 = 10 - P.log2L;  // log2(rows per tile)
+    extern __shared__ uint2 sh_map_all[];  // [warps][rows_per_chunk * (k + kb)]
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t kk = P.k + P.kb;
-    const uint32_t n_map = (1u << rpt_log2) * kk;
-    if (tid == 0) sh_nnz = 0;
+    const uint32_t rows = kTile >> P.log2L;  // input rows per chunk
+    const uint32_t n_map = rows * kk;
+    uint2* sh_map = sh_map_all + warp * n_map;
+    const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
+    const bool vec_ok = (P.d & 3u) == 0;
     uint32_t my_nnz = 0;
 
-    uint32_t tile = blockIdx.x;
-    float4 v = tile < ntiles ? load_tile4(x, (uint64_t)tile * kTile + 4 * tid, P.d)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-    for (; tile < ntiles; tile += gridDim.x) {
-        const uint32_t next = tile + gridDim.x;
-        float4 vn = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (next < ntiles) vn = load_tile4(x, (uint64_t)next * kTile + 4 * tid, P.d);
-        const uint64_t row0 = ((uint64_t)tile * kTile) >> P.log2L;
-
-        // 1. row maps of the tile's rows
-        if (tid < n_map) {
-            uint32_t r = tid / kk, jj = tid - r * kk;
-            uint32_t dom = jj < P.k ? 0u : 1u;
-            uint32_t j = dom ? jj - P.k : jj;
-            sh_map[tid] = row_map(P.seed, dom, j, row0 + r, dom ? P.S_B : P.S_Y, P.L);
-        }
-        // 2. nonzero mask words (coordinate 4*tid+e of the tile = bit (4*lane+e)&31
-        //    of tile word (4*tid+e)>>5 = warp*4 + lane/8)
-        uint32_t nib = (v.x != 0.f ? 1u : 0u) | (v.y != 0.f ? 2u : 0u) | (v.z != 0.f ? 4u : 0u) |
-                       (v.w != 0.f ? 8u : 0u);
-        my_nnz += __popc(nib);
-        uint32_t wv = nib << (4 * (lane & 7));
-        wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
-        wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
-        wv |= __shfl_xor_sync(0xffffffffu, wv, 4);
-        if ((lane & 7) == 0) sh_src[warp * 4 + (lane >> 3)] = wv;
-        __syncthreads();
-
-        // 3. Bloom filter: thread (j = tid/32, tile word gw = tid%32)
-        if (tid < 32 * P.kb) {
-            const uint32_t j = tid >> 5, gw = tid & 31;
-            const uint32_t r = gw >> P.log2nw, w = gw & (P.nw - 1);
-            const uint2 mp = sh_map[r * kk + P.k + j];
-            const uint32_t sb = (32 * w + P.L - map_bias(mp)) & (P.L - 1);  // (32w - bias) mod L
-            const uint32_t sw = sb >> 5, sh = sb & 31;
-            const uint32_t lo = sh_src[(r << P.log2nw) + sw];
-            const uint32_t hi = sh_src[(r << P.log2nw) + ((sw + 1) & (P.nw - 1))];
-            const uint32_t dst = sh ? (lo >> sh) | (hi << (32 - sh)) : lo;
-            if (dst) atomicOr(bitmap + (uint64_t)mp.x * P.nw + w, dst);
-        }
-        // 4. Count Sketch
-        if (nib) {
-            const uint32_t q = 4 * tid;
-            const uint32_t r = q >> P.log2L, t0 = q & (P.L - 1);
-            const float xv[4] = {v.x, v.y, v.z, v.w};
-            for (uint32_t j = 0; j < P.k; j++) {
-                const uint2 mp = sh_map[r * kk + j];
-                const float g = map_sign(mp);
-                const uint64_t base = (uint64_t)mp.x << P.log2L;
-                const uint32_t b = map_bias(mp);
+    for (uint64_t chunk = blockIdx.x * (uint64_t)kCompressWarps + warp; chunk < nchunks;
+         chunk += (uint64_t)gridDim.x * kCompressWarps) {
+        const uint64_t base = chunk * kTile;
+        // 1. loads (lane owns float4 groups g = lane + 32 q)
+        float4 v[8];
 #pragma unroll
-                for (int e = 0; e < 4; e++)
-                    if (nib & (1u << e))
-                        atomicAdd(counters + base + ((t0 + e + b) & (P.L - 1)), g * xv[e]);
+        for (int q = 0; q < 8; q++) {
+            const uint64_t p0 = base + 4 * (lane + 32 * q);
+            if (p0 + 3 < P.d && vec_ok) {
+                v[q] = __ldcs(reinterpret_cast<const float4*>(x + p0));
+            } else {
+                v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (p0 < P.d) v[q].x = x[p0];
+                if (p0 + 1 < P.d) v[q].y = x[p0 + 1];
+                if (p0 + 2 < P.d) v[q].z = x[p0 + 2];
+                if (p0 + 3 < P.d) v[q].w = x[p0 + 3];
             }
         }
-        __syncthreads();
-        v = vn;
+        // 2. row maps of the chunk's rows (overlaps the loads)
+        const uint64_t row0 = base >> P.log2L;
+        for (uint32_t a = lane; a < n_map; a += 32) {
+            const uint32_t r = a / kk, jj = a - r * kk;
+            const uint32_t dom = jj < P.k ? 0u : 1u;
+            sh_map[a] = row_map(P.seed, dom, dom ? jj - P.k : jj, row0 + r, dom ? P.S_B : P.S_Y, P.L);
+        }
+        __syncwarp();
+        // 3. nonzero words: group g = lane + 32q covers coordinates 4g..4g+3, i.e. bits
+        //    4*(lane%8).. of word g/8 = 4q + lane/8
+        uint32_t nibs = 0, word = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const uint32_t nib = (v[q].x != 0.f ? 1u : 0u) | (v[q].y != 0.f ? 2u : 0u) |
+                                 (v[q].z != 0.f ? 4u : 0u) | (v[q].w != 0.f ? 8u : 0u);
+            nibs |= nib << (4 * q);
+            uint32_t wv = nib << (4 * (lane & 7));
+            wv |= __shfl_xor_sync(kFullMask, wv, 1);
+            wv |= __shfl_xor_sync(kFullMask, wv, 2);
+            wv |= __shfl_xor_sync(kFullMask, wv, 4);
+            const uint32_t t = __shfl_sync(kFullMask, wv, 8 * (lane & 3));
+            if ((lane >> 2) == (uint32_t)q) word = t;
+        }
+        my_nnz += __popc(nibs);
+        if (!__any_sync(kFullMask, nibs != 0)) continue;
+        // 4. Bloom filter, lane w = word w of the chunk
+        {
+            const uint32_t r = lane >> P.log2nw, w = lane & (P.nw - 1);
+            const uint32_t seg = r << P.log2nw;
+            for (uint32_t j = 0; j < P.kb; j++) {
+                const uint2 mp = sh_map[r * kk + P.k + j];
+                const uint32_t sb = (32 * w + P.L - map_bias(mp)) & (P.L - 1);  // (32w - bias) mod L
+                const uint32_t sw = sb >> 5, sh = sb & 31;
+                const uint32_t lo = __shfl_sync(kFullMask, word, seg + sw);
+                const uint32_t hi = __shfl_sync(kFullMask, word, seg + ((sw + 1) & (P.nw - 1)));
+                const uint32_t dst = sh ? (lo >> sh) | (hi << (32 - sh)) : lo;
+                if (dst) atomicOr(bitmap + (uint64_t)mp.x * P.nw + w, dst);
+            }
+        }
+        // 5. Count Sketch
+        if (nibs) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const uint32_t nib = (nibs >> (4 * q)) & 0xfu;
+                if (!nib) continue;
+                const uint32_t c0 = 4 * (lane + 32 * q);  // coordinate within the chunk
+                const uint32_t r = c0 >> P.log2L, t0 = c0 & (P.L - 1);
+                const float xv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+                for (uint32_t j = 0; j < P.k; j++) {
+                    const uint2 mp = sh_map[r * kk + j];
+                    const float g = map_sign(mp);
+                    const uint64_t rb = (uint64_t)mp.x << P.log2L;
+                    const uint32_t b = map_bias(mp);
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        if (nib & (1u << e)) atomicAdd(counters + rb + ((t0 + e + b) & (P.L - 1)), g * xv[e]);
+                }
+            }
+        }
+        __syncwarp();  // sh_map is rewritten by the next chunk
     }
     if (nnz_out) {
-        for (int o = 16; o; o >>= 1) my_nnz += __shfl_xor_sync(0xffffffffu, my_nnz, o);
-        if (lane == 0 && my_nnz) atomicAdd(&sh_nnz, (unsigned long long)my_nnz);
-        __syncthreads();
-        if (tid == 0 && sh_nnz) atomicAdd(nnz_out, sh_nnz);
+        for (int o = 16; o; o >>= 1) my_nnz += __shfl_xor_sync(kFullMask, my_nnz, o);
+        if (lane == 0 && my_nnz) atomicAdd(nnz_out, (unsigned long long)my_nnz);
     }
 }
 
 void launch_compress_dense(const KParams& P, const float* x, uint32_t* bitmap, float* counters,
                            unsigned long long* nnz_out, cudaStream_t s) {
-    uint32_t ntiles = (uint32_t)((P.d + kTile - 1) / kTile);
-    uint32_t blocks = std::min<uint32_t>(ntiles, (uint32_t)num_sms() * 8);
-    k_compress_dense<<<blocks, kCompressThreads, 0, s>>>(P, x, bitmap, counters, nnz_out);
+    const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
+    const size_t smem = (size_t)kCompressWarps * (kTile >> P.log2L) * (P.k + P.kb) * sizeof(uint2);
+    static int per_sm[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !per_sm[dev]) {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_compress_dense, kCompressThreads,
+                                                      kCompressWarps * 32 * 2 * kMaxK * sizeof(uint2));
+        per_sm[dev] = std::max(1, n);
+    }
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((nchunks + kCompressWarps - 1) / kCompressWarps,
+                                                         (uint64_t)num_sms() * (dev < 64 ? per_sm[dev] : 2));
+    k_compress_dense<<<blocks, kCompressThreads, smem, s>>>(P, x, bitmap, counters, nnz_out);
     count_launch();
 }
 

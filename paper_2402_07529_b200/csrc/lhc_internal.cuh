@@ -73,23 +73,32 @@ struct __align__(16) CellState {
 struct Ctrl {
     unsigned long long n_cand;  // written by the query scan
     uint32_t overflow;
-    // Per-round counters, triple-buffered by round index r % 3: round r appends
-    // its new frontier cells after the current segment through qcnt[r % 3] and
-    // counts its peels in pcnt[r % 3]; both are read by every block after the
-    // grid barrier that ends round r (when they are final) and reset by block 0
-    // during round r + 2, when no block reads or writes them any more.
-    uint32_t qcnt[3];
-    uint32_t pcnt[3];
-    uint32_t pad;
+    // Per-round counter, triple-buffered by round index r % 3: round r appends its
+    // new frontier entries after the current segment through the low 32 bits of
+    // rc[r % 3] and counts its peels in the high 32 bits; every block reads it
+    // (one 64-bit load) after the grid barrier that ends round r, when it is
+    // final, and block 0 resets it during round r + 2, when nobody uses it.
+    unsigned long long rc[3];
+    uint32_t rounds_dbg;
+    // instrumentation (device globaltimer ns): t[0..3] phase starts, t[3 + r] start of
+    // round r, t[kCtrlTimes-1] end of rounds; fsize[r] = queue segment of round r
+    unsigned long long t[128];
+    uint32_t fsize[128];
 };
+constexpr int kCtrlTimes = 128;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Sub-allocation of the decompress workspace.
 struct WsLayout {
-    size_t tabS, tabB, tile_cnt, chunk_off, cells, claim, frontier, ctrl, total;
-    uint32_t ntiles, nchunks;
+    size_t tabS, gmask, chunk_cnt, chunk_off, cta_total, cells, claim, ccell, frontier, ctrl, total;
+    uint32_t nchunks;
 };
 
-constexpr uint32_t kQueryTile = 32 * kTile;  // coordinates per query CTA tile (32 chunks)
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -72,6 +72,24 @@ class Decoder:
         return self.idx[:n], self.val[:n], self.peeled[:n]
 
 
+def owned_workers(workers: int, rank: int, world: int) -> list[int]:
+    """Workers a rank holds: w % world == rank (every worker exactly once)."""
+    return [w for w in range(workers) if w % world == rank]
+
+
+def exchange_handles(handle: bytes, offset: int, group=None):
+    """All-gather every rank's (64-byte IPC handle, offset) over the process group;
+    returns (handles, offsets) in rank order."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (bytes(handle), int(offset)), group=group)
+    if any(len(g[0]) != 64 for g in gathered):
+        raise ValueError("IPC handles must be 64 bytes")
+    return [g[0] for g in gathered], [g[1] for g in gathered]
+
+
 class PeerComm:
     """NVLink P2P all-reduce of a Sketch across the ranks of a process group
     (one process per GPU).  Construction is collective."""
@@ -86,10 +104,9 @@ class PeerComm:
         self.sketch = Sketch(p, device)
         torch.cuda.synchronize()
         handle, offset = L.lhc_ipc_handle(self.sketch.buf)
-        gathered = [None] * self.world
-        dist.all_gather_object(gathered, (handle, offset), group=group)
-        self.handle = L.lhc_comm_create(self.rank, self.world, [g[0] for g in gathered],
-                                        [g[1] for g in gathered], self.sketch.buf, p)
+        handles, offsets = exchange_handles(handle, offset, group)
+        self.handle = L.lhc_comm_create(self.rank, self.world, handles, offsets,
+                                        self.sketch.buf, p)
         dist.barrier(group=group)
 
     def allreduce(self, stream=None):

@@ -1,0 +1,86 @@
+"""Multi-GPU parity worker (launched by tests/test_gpu_multi.py under torchrun).
+
+Each rank compresses the workers it owns (w % world == rank) into the NVLink
+communication buffer, sketch_allreduce makes every rank's sketch the OR/sum over
+all ranks, and every rank decodes.  Rank 0 checks against the CPU oracle; all
+ranks check that their aggregated sketch bytes and decoded indices/flags are
+identical across ranks.  Exit code 0 = pass.
+"""
+import os
+import sys
+import zlib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from lhc_inputs import config  # noqa: E402
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "ncf"
+    law = sys.argv[2] if len(sys.argv) > 2 else "dyadic"
+    steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    import paper_2402_07529_b200 as lhc
+
+    wl = config(name, law=law)
+    if name == "tiny":
+        wl = config(name, law=law, workers=max(world, 2))
+    s = lhc.size_workload(wl.d, wl.density, wl.workers)
+    p = lhc.params(wl.d, s.m, s.c, 3, 0, 1024, 0x1DC0DE)
+    mine = [w for w in range(wl.workers) if w % world == rank]
+    xs = [torch.from_numpy(wl.dense(w)).to(dev) for w in mine]
+    comm = lhc.PeerComm(p)
+    run = lhc.LosslessAllReduce(p, min(wl.d, int(s.n_cand_expected * 1.5) + 4096),
+                                local_workers=len(xs), comm=comm, device=dev)
+    for _ in range(steps):  # repeated steps exercise the barrier epochs
+        dec = run.step(xs)
+    torch.cuda.synchronize()
+    st = dec.read_stats()
+    n = st["n_cand"]
+    B = run.sketch.bitmap.cpu().numpy().view(np.uint32)
+    Y = run.sketch.counters.cpu().numpy()
+    idx = dec.idx[:n].cpu().numpy().view(np.uint32)
+    peeled = dec.peeled[:n].cpu().numpy()
+    val = dec.val[:n].cpu().numpy()
+    # identical on every rank (the aggregate is reduced once per slice, then copied)
+    digest = torch.tensor([zlib.crc32(a.tobytes()) for a in (B, Y, idx, peeled)] + [st["rounds"]],
+                          dtype=torch.int64, device=dev)
+    allg = [torch.zeros_like(digest) for _ in range(world)]
+    dist.all_gather(allg, digest)
+    ok = all(torch.equal(allg[0], a) for a in allg)
+    if rank == 0:
+        import oracle
+
+        op = oracle.params(p.d, p.m, p.c, p.k, p.k_bloom, p.L, p.seed)
+        Bo, Yo, ref = oracle.pipeline(op, [wl.dense(w) for w in range(wl.workers)], dense=False)
+        ok &= np.array_equal(B, Bo)
+        if law == "dyadic":
+            ok &= np.array_equal(Y.astype(np.float64), Yo)
+            ok &= np.array_equal(val.astype(np.float64), ref.val)
+        else:
+            ok &= bool(np.all(np.abs(Y - Yo) <= 1e-7 + 1e-5 * np.abs(Yo)))
+            ok &= bool(np.all(np.abs(val - ref.val) <= 1e-7 + 1e-5 * np.abs(ref.val)))
+        ok &= n == ref.stats.n_cand and np.array_equal(idx, ref.cand)
+        ok &= np.array_equal(peeled.astype(bool), ref.peeled)
+        ok &= st["rounds"] == ref.stats.rounds and st["success"] == ref.stats.success
+        print(f"mgpu {name} world={world} n_cand={n} rounds={st['rounds']} ok={ok}", flush=True)
+    if not ok:
+        print(f"rank {rank}: mismatch (digests {[a.tolist() for a in allg]})", flush=True)
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,88 @@
+"""world_size-2 gloo tests of the N>1 host logic on CPU (-m "not gpu").
+
+The GPU exchange itself (NVLink P2P) needs GPUs; here the same orchestration
+runs over a real gloo process group: worker ownership, the IPC-handle exchange
+protocol, and the homomorphic exchange semantics (OR of bitmaps, sum of
+counters across ranks == the single-process aggregate), with the
+oracle standing in for the per-rank compression."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from lhc_inputs import config
+        from paper_2402_07529_b200.pipeline import exchange_handles, owned_workers
+        from paper_2402_07529_b200.sizing import size_workload
+
+        # ownership covers every worker exactly once
+        mine = owned_workers(8, rank, world)
+        allw = [None] * world
+        dist.all_gather_object(allw, mine)
+        assert sorted(sum(allw, [])) == list(range(8))
+
+        # handle exchange protocol (fake 64-byte handles)
+        h = bytes([rank]) * 64
+        handles, offsets = exchange_handles(h, 256 * rank)
+        assert handles == [bytes([r]) * 64 for r in range(world)]
+        assert offsets == [256 * r for r in range(world)]
+
+        # homomorphic exchange: per-rank sketches OR/summed across ranks
+        wl = config("tiny", law="dyadic", workers=4, d=60_000)
+        s = size_workload(wl.d, wl.density, wl.workers)
+        p = oracle.params(wl.d, s.m, s.c, 3, 0, 1024, 77)
+        B, Y = oracle.empty_sketch(p)
+        for w in owned_workers(wl.workers, rank, world):
+            oracle.compress_dense(p, wl.dense(w), B, Y)
+        Yt = torch.from_numpy(Y.copy())
+        dist.all_reduce(Yt)
+        Bs = [torch.zeros(len(B), dtype=torch.int32) for _ in range(world)]
+        dist.all_gather(Bs, torch.from_numpy(B.view(np.int32).copy()))
+        Bor = np.bitwise_or.reduce(np.stack([b.numpy().view(np.uint32) for b in Bs]), axis=0)
+        Bref, Yref, ref = oracle.pipeline(p, [wl.dense(w) for w in range(wl.workers)])
+        assert np.array_equal(Bor, Bref)
+        assert np.array_equal(Yt.numpy(), Yref)
+        dec = oracle.decompress(p, Bor, Yt.numpy())
+        assert dec.stats.success and np.array_equal(dec.dense, ref.dense)
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_exchange(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert all(v == "ok" for v in res.values()), res

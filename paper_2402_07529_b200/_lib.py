@@ -15,6 +15,8 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblhc.so")
+# experiment hook: load another build of the same sources (never a fallback)
+LIB_PATH = os.environ.get("LHC_LIB", LIB_PATH)
 
 LHC_OK, LHC_EINVAL, LHC_ECAPACITY, LHC_ECUDA, LHC_ECOMM = 0, 1, 2, 3, 4
 

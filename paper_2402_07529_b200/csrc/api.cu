@@ -92,8 +92,7 @@ WsLayout ws_layout(const KParams& P, uint64_t cap) {
     W.chunk_off = o; o = align_up(o + (size_t)W.nchunks * sizeof(uint32_t), 256);
     W.cta_total = o; o = align_up(o + kMaxQueryCtas * sizeof(uint32_t), 256);
     W.cells = o;     o = align_up(o + P.c * sizeof(CellState), 256);
-    W.claim = o;     o = align_up(o + std::max<uint64_t>(cap, 1) * sizeof(uint32_t), 256);
-    W.ccell = o;     o = align_up(o + peel_ccell_bytes(P.k, cap), 256);
+    W.claim = o;     o = align_up(o + (std::max<uint64_t>(cap, 1) + 31) / 32 * sizeof(uint32_t), 256);
     W.frontier = o;  o = align_up(o + P.c * sizeof(uint2), 256);
     W.total = o;
     return W;
@@ -206,7 +205,6 @@ int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* 
     uint32_t* cta_total = reinterpret_cast<uint32_t*>(b + W.cta_total);
     CellState* cells = reinterpret_cast<CellState*>(b + W.cells);
     uint32_t* claim = reinterpret_cast<uint32_t*>(b + W.claim);
-    uint32_t* ccell = reinterpret_cast<uint32_t*>(b + W.ccell);
     uint2* frontier = reinterpret_cast<uint2*>(b + W.frontier);
 
     if (query_max_ctas() > kMaxQueryCtas) return set_error(LHC_ECUDA, "device too large for the query grid");
@@ -215,7 +213,7 @@ int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* 
     cudaError_t e = launch_query(P, bitmap, tabS, gmask, chunk_cnt, chunk_off, cta_total, cap_cand,
                                  out_idx, ctrl, stats, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "query launch: %s", cudaGetErrorString(e));
-    e = launch_peel(P, counters, tabS, out_idx, cap_cand, cells, claim, ccell, frontier, ctrl,
+    e = launch_peel(P, counters, tabS, out_idx, cap_cand, cells, claim, frontier, ctrl,
                     out_val, out_peeled, stats, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
     if (out_dense) launch_densify(P, gmask, chunk_off, cap_cand, out_val, out_dense, s);

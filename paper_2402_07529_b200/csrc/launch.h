@@ -35,9 +35,8 @@ void launch_densify(const KParams& P, const uint32_t* gmask, const uint32_t* chu
 // peeling decoder (peel.cu)
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* cand, uint64_t cap, CellState* cells, uint32_t* claim,
-                        uint32_t* ccell, uint2* frontier, Ctrl* ctrl, float* out_val,
-                        uint8_t* out_peeled, lhc_stats* stats, cudaStream_t s);
-size_t peel_ccell_bytes(uint32_t k, uint64_t cap);
+                        uint2* frontier, Ctrl* ctrl, float* out_val, uint8_t* out_peeled,
+                        lhc_stats* stats, cudaStream_t s);
 
 WsLayout ws_layout(const KParams& P, uint64_t cap);
 

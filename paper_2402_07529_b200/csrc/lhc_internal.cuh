@@ -95,7 +95,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // Sub-allocation of the decompress workspace.
 struct WsLayout {
-    size_t tabS, gmask, chunk_cnt, chunk_off, cta_total, cells, claim, ccell, frontier, ctrl, total;
+    size_t tabS, gmask, chunk_cnt, chunk_off, cta_total, cells, claim, frontier, ctrl, total;
     uint32_t nchunks;
 };
 

@@ -4,16 +4,15 @@
 //
 // One cooperative, persistent kernel (grid-wide barriers between phases) so that
 // the whole round loop runs on the device with no host round trips:
-//   init     cell state {key = 0, R = Y}; claim[s] = unclaimed
-//   insert   every candidate s computes its k cells once (cached in ccell[s]) and
-//            adds (2^32 + s) to each cell's key: degree and slot sum in one
-//            64-bit reduction
+//   init     cell state {key = 0, R = Y}; claim bits cleared
+//   insert   every candidate s adds (2^32 + s) to the key of each of its k cells:
+//            degree and slot sum in one 64-bit reduction
 //   F0       every cell of degree one is appended to the frontier queue as the
 //            pair (cell, its only candidate)
 //   rounds   (synchronous, reading R10) for every queue entry (e, s) of the
-//            previous round's segment: claim s (atomicCAS — a candidate can be the
-//            only one left in several cells; a stale entry whose candidate was
-//            peeled meanwhile fails the claim), read val = sign * R[e] ("mapped by
+//            previous round's segment: claim s (fetch-or of its bit — a candidate can
+//            be the only one left in several cells; a stale entry whose candidate
+//            was peeled meanwhile fails the claim), read val = sign * R[e] ("mapped by
 //            only one non-zero parameter"; "X_i can be deduced as
 //            g_j(i) * Y_h_j(i)"), and subtract sign_j * val and (2^32 + s) from all
 //            k cells of s ("deducting Y_h_j(i) by g_j(i) * X_i").  A cell
@@ -33,10 +32,10 @@ namespace cg = cooperative_groups;
 
 namespace lhc {
 
-constexpr int kPeelThreads = 512;
-constexpr uint32_t kUnclaimed = 0xffffffffu;
-
-__host__ __device__ constexpr uint32_t ccell_stride(uint32_t k) { return k < 4 ? 4u : 8u; }
+#ifndef LHC_PEEL_THREADS
+#define LHC_PEEL_THREADS 512
+#endif
+constexpr int kPeelThreads = LHC_PEEL_THREADS;
 
 __device__ __forceinline__ uint32_t cand_cell(const KParams& P, const uint2* __restrict__ tabS,
                                               uint32_t p, uint32_t j, uint32_t* neg) {
@@ -45,6 +44,23 @@ __device__ __forceinline__ uint32_t cand_cell(const KParams& P, const uint2* __r
     const uint2 mp = __ldg(tabS + i * P.k + j);
     *neg = mp.y >> 31;
     return (mp.x << P.log2L) + ((t + map_bias(mp)) & (P.L - 1));  // c < 2^32
+}
+
+// Loads that must stay where they are written (issued before a dependent branch).
+__device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_nc_u2(const uint2* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+    float v;
+    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
 }
 
 // Block-aggregated append of the pairs in sh_q to the queue segment that starts
@@ -66,16 +82,18 @@ template <int KT>
 __global__ void __launch_bounds__(kPeelThreads)
 k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
        const uint32_t* __restrict__ cand, uint64_t cap, CellState* cells, uint32_t* claim,
-       uint32_t* __restrict__ ccell, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
-       uint8_t* __restrict__ out_peeled, lhc_stats* stats) {
+       uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val, uint8_t* __restrict__ out_peeled,
+       lhc_stats* stats) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint2 sh_q[kPeelThreads * kMaxK];
+    constexpr uint32_t NJ = KT ? KT : kMaxK;
+    // a peel appends at most k - 1 cells (the pure cell is never appended):
+    // kPeelThreads * max(1, k - 1) entries of dynamic shared memory
+    extern __shared__ uint2 sh_q[];
     __shared__ uint32_t sh_n, sh_base, sh_peeled;
     const uint32_t k = KT ? (uint32_t)KT : P.k;
-    const uint32_t cs = ccell_stride(k);
 
     const uint64_t n_c = *(volatile unsigned long long*)&ctrl->n_cand;
-    if (n_c > cap) {  // overflow: nothing is peeled (stats.overflow set by the query scan)
+    if (n_c > cap) {  // overflow: nothing is peeled (stats.overflow set by the query)
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             stats->n_peeled = 0;
             stats->rounds = 0;
@@ -89,37 +107,31 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     if (threadIdx.x == 0) { sh_n = 0; sh_peeled = 0; }
     if (timer) ctrl->t[0] = globaltimer();
 
-    // init
-    for (uint64_t e = gtid; e < P.c; e += gstride) {
+    // init: cell state {0, Y} (4 cells per thread and pass: 4 loads in flight),
+    // claim bits cleared
+    for (uint64_t e0 = gtid * 4; e0 < P.c; e0 += gstride * 4) {  // c is a multiple of 32
+        const float4 y = __ldcs(reinterpret_cast<const float4*>(counters + e0));
         CellState st;
         st.key = 0ull;
-        st.R = __ldcs(counters + e);
         st.pad = 0u;
-        cells[e] = st;
+        st.R = y.x; cells[e0] = st;
+        st.R = y.y; cells[e0 + 1] = st;
+        st.R = y.z; cells[e0 + 2] = st;
+        st.R = y.w; cells[e0 + 3] = st;
     }
-    for (uint64_t s = gtid; s < n_c; s += gstride) claim[s] = kUnclaimed;
+    for (uint64_t w = gtid; w < (n_c + 31) / 32; w += gstride) claim[w] = 0u;
     grid.sync();
     if (timer) ctrl->t[1] = globaltimer();
 
-    // insert: cells of every candidate (cached), degree and slot sum of every cell
+    // insert: degree and slot sum of every cell
     for (uint64_t s = gtid; s < n_c; s += gstride) {
-        const uint32_t p = cand[s];
-        uint32_t ev[KT ? KT : kMaxK];
-        uint32_t negs = 0;
+        const uint32_t p = __ldg(cand + s);
 #pragma unroll
-        for (uint32_t j = 0; j < (KT ? (uint32_t)KT : (uint32_t)kMaxK); j++) {
+        for (uint32_t j = 0; j < NJ; j++) {
             if (!KT && j >= k) break;
             uint32_t neg;
-            ev[j] = cand_cell(P, tabS, p, j, &neg);
-            negs |= neg << j;
-            atomicAdd(&cells[ev[j]].key, (1ull << 32) + s);
-        }
-        uint32_t* dst = ccell + s * cs;
-        if (KT == 3) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(ev[0], ev[1], ev[2], negs);
-        } else {
-            for (uint32_t j = 0; j < k; j++) dst[j] = ev[j];
-            dst[cs - 1] = negs;
+            const uint32_t e = cand_cell(P, tabS, p, j, &neg);
+            atomicAdd(&cells[e].key, (1ull << 32) + s);
         }
     }
     grid.sync();
@@ -155,39 +167,50 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
             if (f < f_end) {
                 const uint2 ent = frontier[f];
                 const uint32_t e = ent.x, s = ent.y;
-                // independent: the claim, the candidate's cells and the pure cell's residual
-                const uint32_t* src = ccell + (uint64_t)s * cs;
-                uint32_t ev[KT ? KT : kMaxK];
-                uint32_t negs;
-                if (KT == 3) {
-                    const uint4 c4 = __ldcg(reinterpret_cast<const uint4*>(src));
-                    ev[0] = c4.x; ev[1] = c4.y; ev[2] = c4.z; negs = c4.w;
-                } else {
-                    for (uint32_t j = 0; j < k; j++) ev[j] = __ldcg(src + j);
-                    negs = __ldcg(src + cs - 1);
+                // issued back to back (volatile loads are not sunk into the branch):
+                // the candidate, the pure cell's residual and the claim (fetch-or of the
+                // candidate's bit: a candidate can be the only one left in several
+                // cells; a stale entry finds its bit already set), then the row maps
+                const uint32_t p = ld_nc_u32(cand + s);
+                const float Re = ld_cg_f32(&cells[e].R);
+                const uint32_t bit = 1u << (s & 31);
+                const uint32_t old = atomicOr(claim + (s >> 5), bit);
+                const uint2* row = tabS + (uint64_t)(p >> P.log2L) * k;
+                uint2 mp[NJ];
+#pragma unroll
+                for (uint32_t j = 0; j < NJ; j++) {
+                    if (!KT && j >= k) break;
+                    mp[j] = ld_nc_u2(row + j);
                 }
-                const float Re = __ldcg(&cells[e].R);
-                if (atomicCAS(claim + s, kUnclaimed, 1u) == kUnclaimed) {
+                if (!(old & bit)) {
+                    const uint32_t t = p & (P.L - 1);
+                    uint32_t ev[NJ];
                     float ge = 1.f;
 #pragma unroll
-                    for (uint32_t j = 0; j < (KT ? (uint32_t)KT : (uint32_t)kMaxK); j++) {
+                    for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
-                        if (ev[j] == e) ge = ((negs >> j) & 1u) ? -1.f : 1.f;
+                        ev[j] = (mp[j].x << P.log2L) + ((t + map_bias(mp[j])) & (P.L - 1));
+                        if (ev[j] == e) ge = map_sign(mp[j]);
                     }
                     const float val = ge * Re;
                     out_val[s] = val;
                     atomicAdd(&sh_peeled, 1u);
+                    // all reductions first (independent), then the queue appends
+                    unsigned long long rest[NJ];
 #pragma unroll
-                    for (uint32_t j = 0; j < (KT ? (uint32_t)KT : (uint32_t)kMaxK); j++) {
+                    for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
                         // the pure cell held only s: nothing reads its state again
                         if (ev[j] == e) continue;
-                        const float g = ((negs >> j) & 1u) ? -1.f : 1.f;
-                        atomicAdd(&cells[ev[j]].R, -g * val);
-                        const unsigned long long rest =
-                            atomicAdd(&cells[ev[j]].key, 0ull - ((1ull << 32) + s)) - ((1ull << 32) + s);
-                        if ((rest >> 32) == 1ull)
-                            sh_q[atomicAdd(&sh_n, 1u)] = make_uint2(ev[j], (uint32_t)rest);
+                        atomicAdd(&cells[ev[j]].R, -map_sign(mp[j]) * val);
+                        rest[j] = atomicAdd(&cells[ev[j]].key, 0ull - ((1ull << 32) + s)) -
+                                  ((1ull << 32) + s);
+                    }
+#pragma unroll
+                    for (uint32_t j = 0; j < NJ; j++) {
+                        if (!KT && j >= k) break;
+                        if (ev[j] != e && (rest[j] >> 32) == 1ull)
+                            sh_q[atomicAdd(&sh_n, 1u)] = make_uint2(ev[j], (uint32_t)rest[j]);
                     }
                 }
             }
@@ -209,14 +232,16 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
 
     // finalize: median estimate of unpeeled candidates
     for (uint64_t s = gtid; s < n_c; s += gstride) {
-        const bool pe = __ldcg(claim + s) != kUnclaimed;
+        const bool pe = (__ldcg(claim + (s >> 5)) >> (s & 31)) & 1u;
         out_peeled[s] = pe ? 1 : 0;
         if (!pe) {
-            const uint32_t* src = ccell + s * cs;
-            const uint32_t negs = src[cs - 1];
-            float v[KT ? KT : kMaxK];
-            for (uint32_t j = 0; j < k; j++)
-                v[j] = (((negs >> j) & 1u) ? -1.f : 1.f) * __ldcg(&cells[src[j]].R);
+            const uint32_t p = __ldg(cand + s);
+            float v[NJ];
+            for (uint32_t j = 0; j < k; j++) {
+                uint32_t neg;
+                const uint32_t e = cand_cell(P, tabS, p, j, &neg);
+                v[j] = (neg ? -1.f : 1.f) * __ldcg(&cells[e].R);
+            }
             for (uint32_t a = 1; a < k; a++) {  // insertion sort of <= 8 values
                 float x = v[a];
                 int b = (int)a - 1;
@@ -234,39 +259,37 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     }
 }
 
-template <int KT>
-static int peel_grid(int dev) {
-    static int cached[64] = {0};
-    if (dev < 64 && cached[dev]) return cached[dev];
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel<KT>, kPeelThreads, 0);
-    int g = std::max(1, per_sm) * num_sms();
-    if (dev < 64) cached[dev] = g;
-    return g;
-}
+static size_t peel_smem(uint32_t k) { return (size_t)kPeelThreads * (k > 1 ? k - 1 : 1) * sizeof(uint2); }
 
-size_t peel_ccell_bytes(uint32_t k, uint64_t cap) {
-    return (size_t)ccell_stride(k) * 4 * std::max<uint64_t>(cap, 1);
+template <int KT>
+static int peel_grid(int dev, uint32_t k) {
+    static int cached[64][kMaxK + 1] = {};
+    if (dev < 64 && cached[dev][k]) return cached[dev][k];
+    cudaFuncSetAttribute(k_peel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)peel_smem(k));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel<KT>, kPeelThreads, peel_smem(k));
+    int g = std::max(1, per_sm) * num_sms();
+    if (dev < 64) cached[dev][k] = g;
+    return g;
 }
 
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* cand, uint64_t cap, CellState* cells, uint32_t* claim,
-                        uint32_t* ccell, uint2* frontier, Ctrl* ctrl, float* out_val,
-                        uint8_t* out_peeled, lhc_stats* stats, cudaStream_t s) {
+                        uint2* frontier, Ctrl* ctrl, float* out_val, uint8_t* out_peeled,
+                        lhc_stats* stats, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     KParams Pc = P;
     void* args[] = {(void*)&Pc,    (void*)&counters, (void*)&tabS,     (void*)&cand,
-                    (void*)&cap,   (void*)&cells,    (void*)&claim,    (void*)&ccell,
-                    (void*)&frontier, (void*)&ctrl,  (void*)&out_val,  (void*)&out_peeled,
-                    (void*)&stats};
+                    (void*)&cap,   (void*)&cells,    (void*)&claim,    (void*)&frontier,
+                    (void*)&ctrl,  (void*)&out_val,  (void*)&out_peeled, (void*)&stats};
     cudaError_t err;
     if (P.k == 3)
-        err = cudaLaunchCooperativeKernel((const void*)k_peel<3>, dim3(peel_grid<3>(dev)),
-                                          dim3(kPeelThreads), args, 0, s);
+        err = cudaLaunchCooperativeKernel((const void*)k_peel<3>, dim3(peel_grid<3>(dev, 3)),
+                                          dim3(kPeelThreads), args, peel_smem(3), s);
     else
-        err = cudaLaunchCooperativeKernel((const void*)k_peel<0>, dim3(peel_grid<0>(dev)),
-                                          dim3(kPeelThreads), args, 0, s);
+        err = cudaLaunchCooperativeKernel((const void*)k_peel<0>, dim3(peel_grid<0>(dev, P.k)),
+                                          dim3(kPeelThreads), args, peel_smem(P.k), s);
     count_launch();
     return err;
 }

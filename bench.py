@@ -292,9 +292,16 @@ def main():
             else:
                 nccl_allreduce()
         mark("allreduce")
-        run.decoder(run.sketch)
+        dec = run.decoder
+        dec.query(run.sketch)
         cnt()
-        mark("decode")
+        mark("query")
+        dec.peel(run.sketch)
+        cnt()
+        mark("peel")
+        dec.densify()
+        cnt()
+        mark("densify")
 
     def barrier():
         if world > 1:
@@ -313,7 +320,8 @@ def main():
     clocks.start()
     time.sleep(0.3)
     per_step = []
-    phase = {"compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "decode": 0.0}
+    phase = {"compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "query": 0.0, "peel": 0.0,
+             "densify": 0.0}
     compress_launch_ms = []
     launches = [0]
     barrier()
@@ -385,24 +393,49 @@ def main():
             e2e = None
 
     trace('roofline')
-    # ---- roofline of the dominant kernel (compress) ----
-    import json as _json
-
+    # ---- roofline: every step of the path against its bound; the dominant one ----
     peaks = {}
     try:
-        peaks = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     hbm = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
+    nvl = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+    S = int(p.m) // 8 + 4 * int(p.c)
+    n_c = stats["n_cand"]
+    W_loc = len(xs)
+    per_step_ms = {k: v / args.steps for k, v in phase.items()}
     avg_compress_ms = sum(compress_launch_ms) / max(1, len(compress_launch_ms))
-    bytes_compress = 4 * wl.d + (int(p.m) // 8 + 4 * int(p.c))  # read x_w, write the sketch
-    achieved = bytes_compress / (avg_compress_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "k_compress_dense", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                "bytes_per_launch": bytes_compress, "avg_launch_us": avg_compress_ms * 1e3,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+    # algorithmic bytes per launch (Measurement) and launches per step
+    kern = {
+        "k_compress_dense": (4 * wl.d + S, W_loc, avg_compress_ms, hbm, "hbm"),
+        "k_aggregate": ((W_loc + 1) * S, 1 if run.per_worker else 0,
+                        per_step_ms["aggregate"], hbm, "hbm"),
+        "k_allreduce": (2 * (world - 1) / world * S, 1 if world > 1 else 0,
+                        per_step_ms["allreduce"], nvl, "nvlink"),
+        "k_query": (int(p.m) // 8 + 4 * n_c, 1, per_step_ms["query"], hbm, "hbm"),
+        "k_peel": (16 * int(p.c) + 9 * n_c, 1, per_step_ms["peel"], hbm, "hbm"),
+        "k_densify": (4 * wl.d + 4 * n_c, 1, per_step_ms["densify"], hbm, "hbm"),
+    }
+    kernels = {}
+    for name, (byts, nl, ms_l, peak, bound) in kern.items():
+        if nl == 0 or ms_l <= 0:
+            continue
+        ach = byts / (ms_l * 1e-3) / 1e9
+        kernels[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "bytes_per_launch": int(byts),
+                         "avg_launch_us": ms_l * 1e3, "launches_per_step": nl,
+                         "us_per_step": ms_l * 1e3 * nl}
+    dom = max(kernels, key=lambda k: kernels[k]["us_per_step"])
+    roofline = dict(kernels[dom])
+    roofline.update({"kernel": dom, "traffic": None,
+                     "peak_source": hbm_src if roofline["bound"] == "hbm" else
+                     "B200_PROFILING.md measured peer copy 770 GB/s"})
+    roofline = {k: roofline[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic",
+                                         "kernel", "bytes_per_launch", "avg_launch_us",
+                                         "peak_source")}
 
-    trace('cpu baseline')
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ref = run_reference(argparse.Namespace(steps=1, warmup=0, gamma=args.gamma, gpus=1), wl, 0)
@@ -422,11 +455,12 @@ def main():
                        "comm": ("p2p" if comm is not None else "nccl") if world > 1 else "none",
                        "l2": "flushed (256 MB write) between timed steps, outside the events"},
             "roofline": roofline,
+            "kernels": kernels,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches[0],
             "clocks": clocks.summary(),
-            "phases_ms_per_step": {k: v / args.steps for k, v in phase.items()},
+            "phases_ms_per_step": per_step_ms,
             "decode": stats,
         }
         print(json.dumps(line), flush=True)

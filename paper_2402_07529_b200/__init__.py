@@ -23,6 +23,9 @@ from ._lib import (  # noqa: F401
     sketch_compress,
     sketch_compress_coo,
     sketch_decompress,
+    sketch_densify,
+    sketch_peel,
+    sketch_query,
     sketch_hash_rows,
 )
 from .pipeline import Decoder, LosslessAllReduce, PeerComm, Sketch, aggregate  # noqa: F401

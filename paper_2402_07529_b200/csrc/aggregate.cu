@@ -65,4 +65,31 @@ void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* co
     }
 }
 
+// Zero a sketch with L2 evict-last stores: the lines stay L2-resident for the
+// compress reductions that follow (a cold sketch costs one random DRAM sector
+// read per first touch).
+__global__ void __launch_bounds__(256) k_clear(uint4* __restrict__ a, uint64_t na, uint32_t* __restrict__ b,
+                                               uint64_t nb) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t u = tid; u < na; u += stride)
+        asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(a + u), "r"(0u),
+                     "l"(pol) : "memory");
+    for (uint64_t u = tid; u < nb; u += stride)
+        asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(b + u), "r"(0u), "l"(pol)
+                     : "memory");
+}
+
+void launch_clear(uint32_t* bitmap, uint64_t n_words, float* counters, uint64_t c, cudaStream_t s) {
+    // counters: c is a multiple of 32 floats; bitmap words: 16-byte groups + tail
+    const uint64_t units = std::max<uint64_t>(c / 4, n_words / 4);
+    const uint32_t blocks =
+        (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((units + 255) / 256, (uint64_t)num_sms() * 8));
+    k_clear<<<blocks, 256, 0, s>>>(reinterpret_cast<uint4*>(counters), c / 4,
+                                   bitmap, n_words);
+    count_launch();
+}
+
 }  // namespace lhc

@@ -134,11 +134,8 @@ int sketch_clear(const lhc_params* p, uint32_t* bitmap, float* counters, void* s
     reset_launches();
     if (int rc = validate(p)) return rc;
     if (!bitmap || !counters) return set_error(LHC_EINVAL, "NULL sketch buffer");
-    cudaStream_t s = (cudaStream_t)stream;
-    if (cudaMemsetAsync(bitmap, 0, p->m / 8, s) != cudaSuccess ||
-        cudaMemsetAsync(counters, 0, p->c * sizeof(float), s) != cudaSuccess)
-        return check_launch("sketch_clear");
-    return LHC_OK;
+    launch_clear(bitmap, p->m / 32, counters, p->c, (cudaStream_t)stream);
+    return check_launch("sketch_clear");
 }
 
 int sketch_compress(const lhc_params* p, const float* x, uint32_t* bitmap, float* counters,
@@ -180,44 +177,101 @@ int sketch_aggregate(const lhc_params* p, int n_in, const uint32_t* const* bitma
     return check_launch("sketch_aggregate");
 }
 
+namespace {
+struct WsView {
+    KParams P;
+    WsLayout W;
+    Ctrl* ctrl;
+    uint2* tabS;
+    uint32_t *gmask, *chunk_cnt, *chunk_off, *cta_total, *claim;
+    CellState* cells;
+    uint2* frontier;
+};
+
+int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, WsView* v) {
+    if (int rc = validate(p)) return rc;
+    if (!ws) return set_error(LHC_EINVAL, "NULL workspace");
+    if (!aligned16(ws)) return set_error(LHC_EINVAL, "workspace must be 16-byte aligned");
+    if (*cap_cand > p->d) *cap_cand = p->d;
+    v->P = kparams(p);
+    v->W = ws_layout(v->P, *cap_cand);
+    if (ws_bytes < v->W.total)
+        return set_error(LHC_ECAPACITY, "workspace too small: %zu < %zu bytes", ws_bytes, v->W.total);
+    char* b = static_cast<char*>(ws);
+    v->ctrl = reinterpret_cast<Ctrl*>(b + v->W.ctrl);
+    v->tabS = reinterpret_cast<uint2*>(b + v->W.tabS);
+    v->gmask = reinterpret_cast<uint32_t*>(b + v->W.gmask);
+    v->chunk_cnt = reinterpret_cast<uint32_t*>(b + v->W.chunk_cnt);
+    v->chunk_off = reinterpret_cast<uint32_t*>(b + v->W.chunk_off);
+    v->cta_total = reinterpret_cast<uint32_t*>(b + v->W.cta_total);
+    v->cells = reinterpret_cast<CellState*>(b + v->W.cells);
+    v->claim = reinterpret_cast<uint32_t*>(b + v->W.claim);
+    v->frontier = reinterpret_cast<uint2*>(b + v->W.frontier);
+    return LHC_OK;
+}
+}  // namespace
+
+int sketch_query(const lhc_params* p, const uint32_t* bitmap, void* ws, size_t ws_bytes,
+                 uint64_t cap_cand, uint32_t* out_idx, lhc_stats* stats, void* stream) {
+    reset_launches();
+    WsView v;
+    if (int rc = ws_view(p, ws, ws_bytes, &cap_cand, &v)) return rc;
+    if (!bitmap || !stats) return set_error(LHC_EINVAL, "NULL buffer");
+    if (cap_cand && !out_idx) return set_error(LHC_EINVAL, "NULL out_idx");
+    if (query_max_ctas() > kMaxQueryCtas) return set_error(LHC_ECUDA, "device too large for the query grid");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(v.ctrl, 0, sizeof(Ctrl), s) != cudaSuccess) return check_launch("memset");
+    if (cudaMemsetAsync(stats, 0, sizeof(lhc_stats), s) != cudaSuccess) return check_launch("memset");
+    cudaError_t e = launch_query(v.P, bitmap, v.tabS, v.gmask, v.chunk_cnt, v.chunk_off, v.cta_total,
+                                 cap_cand, out_idx, v.ctrl, stats, s);
+    if (e != cudaSuccess) return set_error(LHC_ECUDA, "query launch: %s", cudaGetErrorString(e));
+    return check_launch("sketch_query");
+}
+
+int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_bytes,
+                uint64_t cap_cand, const uint32_t* out_idx, float* out_val, uint8_t* out_peeled,
+                lhc_stats* stats, void* stream) {
+    reset_launches();
+    WsView v;
+    if (int rc = ws_view(p, ws, ws_bytes, &cap_cand, &v)) return rc;
+    if (!counters || !stats) return set_error(LHC_EINVAL, "NULL buffer");
+    if (!aligned16(counters)) return set_error(LHC_EINVAL, "counters must be 16-byte aligned");
+    if (cap_cand && (!out_idx || !out_val || !out_peeled)) return set_error(LHC_EINVAL, "NULL output");
+    cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, cap_cand, v.cells, v.claim,
+                                v.frontier, v.ctrl, out_val, out_peeled, stats, (cudaStream_t)stream);
+    if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
+    return check_launch("sketch_peel");
+}
+
+int sketch_densify(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t cap_cand,
+                   const float* out_val, float* out_dense, void* stream) {
+    reset_launches();
+    WsView v;
+    if (int rc = ws_view(p, ws, ws_bytes, &cap_cand, &v)) return rc;
+    if (!out_dense) return set_error(LHC_EINVAL, "NULL out_dense");
+    if (!aligned16(out_dense)) return set_error(LHC_EINVAL, "out_dense must be 16-byte aligned");
+    if (cap_cand && !out_val) return set_error(LHC_EINVAL, "NULL out_val");
+    launch_densify(v.P, v.gmask, v.chunk_off, cap_cand, out_val, out_dense, (cudaStream_t)stream);
+    return check_launch("sketch_densify");
+}
+
 int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* counters,
                       void* ws, size_t ws_bytes, uint64_t cap_cand, uint32_t* out_idx,
                       float* out_val, uint8_t* out_peeled, float* out_dense, lhc_stats* stats,
                       void* stream) {
+    if (int rc = sketch_query(p, bitmap, ws, ws_bytes, cap_cand, out_idx, stats, stream)) return rc;
+    int n = lhc_last_launch_count();
+    if (int rc = sketch_peel(p, counters, ws, ws_bytes, cap_cand, out_idx, out_val, out_peeled,
+                             stats, stream))
+        return rc;
+    n += lhc_last_launch_count();
+    if (out_dense) {
+        if (int rc = sketch_densify(p, ws, ws_bytes, cap_cand, out_val, out_dense, stream)) return rc;
+        n += lhc_last_launch_count();
+    }
     reset_launches();
-    if (int rc = validate(p)) return rc;
-    if (!bitmap || !counters || !ws || !stats) return set_error(LHC_EINVAL, "NULL buffer");
-    if (cap_cand && (!out_idx || !out_val || !out_peeled)) return set_error(LHC_EINVAL, "NULL output");
-    if (cap_cand > p->d) cap_cand = p->d;
-    if (!aligned16(ws) || !aligned16(counters) || (out_dense && !aligned16(out_dense)))
-        return set_error(LHC_EINVAL, "ws, counters and out_dense must be 16-byte aligned");
-    const KParams P = kparams(p);
-    const WsLayout W = ws_layout(P, cap_cand);
-    if (ws_bytes < W.total)
-        return set_error(LHC_ECAPACITY, "workspace too small: %zu < %zu bytes", ws_bytes, W.total);
-    cudaStream_t s = (cudaStream_t)stream;
-    char* b = static_cast<char*>(ws);
-    Ctrl* ctrl = reinterpret_cast<Ctrl*>(b + W.ctrl);
-    uint2* tabS = reinterpret_cast<uint2*>(b + W.tabS);
-    uint32_t* gmask = reinterpret_cast<uint32_t*>(b + W.gmask);
-    uint32_t* chunk_cnt = reinterpret_cast<uint32_t*>(b + W.chunk_cnt);
-    uint32_t* chunk_off = reinterpret_cast<uint32_t*>(b + W.chunk_off);
-    uint32_t* cta_total = reinterpret_cast<uint32_t*>(b + W.cta_total);
-    CellState* cells = reinterpret_cast<CellState*>(b + W.cells);
-    uint32_t* claim = reinterpret_cast<uint32_t*>(b + W.claim);
-    uint2* frontier = reinterpret_cast<uint2*>(b + W.frontier);
-
-    if (query_max_ctas() > kMaxQueryCtas) return set_error(LHC_ECUDA, "device too large for the query grid");
-    if (cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), s) != cudaSuccess) return check_launch("memset");
-    if (cudaMemsetAsync(stats, 0, sizeof(lhc_stats), s) != cudaSuccess) return check_launch("memset");
-    cudaError_t e = launch_query(P, bitmap, tabS, gmask, chunk_cnt, chunk_off, cta_total, cap_cand,
-                                 out_idx, ctrl, stats, s);
-    if (e != cudaSuccess) return set_error(LHC_ECUDA, "query launch: %s", cudaGetErrorString(e));
-    e = launch_peel(P, counters, tabS, out_idx, cap_cand, cells, claim, frontier, ctrl,
-                    out_val, out_peeled, stats, s);
-    if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
-    if (out_dense) launch_densify(P, gmask, chunk_off, cap_cand, out_val, out_dense, s);
-    return check_launch("sketch_decompress");
+    count_launch(n);
+    return LHC_OK;
 }
 
 }  // extern "C"

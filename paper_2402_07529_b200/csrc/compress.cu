@@ -35,81 +35,162 @@ void launch_hash_rows(const KParams& P, uint32_t dom, uint64_t n_rows, uint2* ou
 //
 // One warp owns a chunk of 1024 consecutive coordinates at a time (1024/L input
 // rows) and needs no block-level synchronisation:
-//   1. eight 128-bit streaming loads per lane (the whole 4 KB chunk in flight);
+//   1. the chunk (4 KB) arrives in the warp's shared-memory ring by a bulk async
+//      copy (cp.async.bulk, the TMA engine, completing on an mbarrier), issued
+//      kStages - 1 chunks ahead, with an L2 evict-first hint: x is read once and
+//      the loads cost no registers;
 //   2. lanes compute the chunk's row maps (one hash per input row and probe,
 //      P:L261 "each batch shares the same index") into a warp-private slice of
 //      shared memory;
-//   3. the chunk's nonzero mask is assembled as 32 words, lane w holding word w
-//      (8-lane OR reductions of per-lane nibbles);
+//   3. word w of the chunk's nonzero mask is ballot(x[32w + lane] != 0); lane w
+//      keeps word w;
 //   4. Bloom filter: for probe j, lane w builds destination word w of its row's
 //      destination row (the rotation by bias_j is two shuffles and a funnel
-//      shift, so a row maps onto exactly one row of B) and issues one atomicOr
-//      if it is nonzero — at most k_bloom*L/32 atomics per input row;
-//   5. Count Sketch: each nonzero adds sign_j * x to its k cells with a
-//      fire-and-forget fp32 reduction (RED.ADD.F32, performed at L2).
+//      shift, so a row maps onto exactly one row of B) and issues one OR
+//      reduction if it is nonzero — at most k_bloom*L/32 per input row;
+//   5. Count Sketch: the chunk's nonzeros are compacted (coordinate, value) and
+//      processed one per lane: sign_j * x is added to each of the k cells with a
+//      fire-and-forget fp32 reduction at L2.
+// The sketch reductions carry an L2 evict-last hint so that the streamed
+// gradient does not evict the sketch lines they accumulate into.
 // ---------------------------------------------------------------------------
-constexpr int kCompressThreads = 256;
-constexpr int kCompressWarps = kCompressThreads / 32;
+#ifndef LHC_COMPRESS_WARPS
+#define LHC_COMPRESS_WARPS 8
+#endif
+#ifndef LHC_COMPRESS_STAGES
+#define LHC_COMPRESS_STAGES 2
+#endif
+constexpr int kCompressWarps = LHC_COMPRESS_WARPS;
+constexpr int kCompressThreads = kCompressWarps * 32;
+constexpr int kStages = LHC_COMPRESS_STAGES;
 constexpr uint32_t kFullMask = 0xffffffffu;
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void red_add(float* a, float v, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void red_or(uint32_t* a, uint32_t v, uint64_t pol) {
+    asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// one thread: expect `bytes` on the barrier and start the bulk copy gmem -> smem
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                          uint64_t pol) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                 " [%0], [%1], %2, [%3], %4;"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// dynamic shared memory per warp: kStages chunk buffers, the compacted nonzeros'
+// coordinates, the row maps, the stage barriers
+__host__ __device__ constexpr size_t compress_warp_smem(uint32_t n_map) {
+    return ((size_t)kStages * kTile * sizeof(float) + kTile * sizeof(uint16_t) +
+            ((n_map * 8 + 15) / 16) * 16 + kStages * sizeof(uint64_t) + 127) / 128 * 128;
+}
 
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ bitmap,
                  float* __restrict__ counters, unsigned long long* __restrict__ nnz_out) {
-    extern __shared__ uint2 sh_map_all[];  // [warps][rows_per_chunk * (k + kb)]
+    extern __shared__ __align__(128) unsigned char sh_all[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t kk = P.k + P.kb;
-    const uint32_t rows = kTile >> P.log2L;  // input rows per chunk
-    const uint32_t n_map = rows * kk;
-    uint2* sh_map = sh_map_all + warp * n_map;
+    const uint32_t n_map = (kTile >> P.log2L) * kk;  // row maps per chunk
+    unsigned char* mine = sh_all + warp * compress_warp_smem(n_map);
+    float* sh_x = reinterpret_cast<float*>(mine);                         // [kStages][kTile]
+    uint16_t* sh_pos = reinterpret_cast<uint16_t*>(sh_x + kStages * kTile);
+    uint2* sh_map = reinterpret_cast<uint2*>(sh_pos + kTile);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sh_map) +
+                                                ((n_map * 8 + 15) / 16) * 16);
     const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
-    const bool vec_ok = (P.d & 3u) == 0;
+    const uint64_t nfull = (uint64_t)P.d / kTile;  // chunks that are whole (bulk-copied)
+    const uint64_t stride = (uint64_t)gridDim.x * kCompressWarps;
+    const uint64_t first = blockIdx.x * (uint64_t)kCompressWarps + warp;
+    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+    const uint32_t lt = (1u << lane) - 1u;
     uint32_t my_nnz = 0;
 
-    for (uint64_t chunk = blockIdx.x * (uint64_t)kCompressWarps + warp; chunk < nchunks;
-         chunk += (uint64_t)gridDim.x * kCompressWarps) {
-        const uint64_t base = chunk * kTile;
-        // 1. loads (lane owns float4 groups g = lane + 32 q)
-        float4 v[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const uint64_t p0 = base + 4 * (lane + 32 * q);
-            if (p0 + 3 < P.d && vec_ok) {
-                v[q] = __ldcs(reinterpret_cast<const float4*>(x + p0));
-            } else {
-                v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (p0 < P.d) v[q].x = x[p0];
-                if (p0 + 1 < P.d) v[q].y = x[p0 + 1];
-                if (p0 + 2 < P.d) v[q].z = x[p0 + 2];
-                if (p0 + 3 < P.d) v[q].w = x[p0 + 3];
+    if (lane == 0) {
+        for (int st = 0; st < kStages; st++) mbar_init(bar + st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // prologue: the first kStages - 1 chunks in flight
+    if (lane == 0) {
+        for (int st = 0; st < kStages - 1; st++) {
+            const uint64_t ch = first + st * stride;
+            if (ch < nfull) bulk_load(sh_x + st * kTile, x + ch * kTile, kTile * 4, bar + st, pol_stream);
+        }
+    }
+    uint32_t it = 0;
+    for (uint64_t chunk = first; chunk < nchunks; chunk += stride, it++) {
+        const uint32_t st = it % kStages;
+        // refill: the stage consumed in the previous iteration takes chunk + (kStages-1) stride
+        {
+            const uint64_t ahead = chunk + (uint64_t)(kStages - 1) * stride;
+            if (lane == 0 && ahead < nfull) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const uint32_t sa = (it + kStages - 1) % kStages;
+                bulk_load(sh_x + sa * kTile, x + ahead * kTile, kTile * 4, bar + sa, pol_stream);
             }
         }
-        // 2. row maps of the chunk's rows (overlaps the loads)
+        const uint64_t base = chunk * kTile;
+        float* cx = sh_x + st * kTile;
+        // row maps of the chunk's rows (overlap the copy)
         const uint64_t row0 = base >> P.log2L;
         for (uint32_t a = lane; a < n_map; a += 32) {
             const uint32_t r = a / kk, jj = a - r * kk;
             const uint32_t dom = jj < P.k ? 0u : 1u;
             sh_map[a] = row_map(P.seed, dom, dom ? jj - P.k : jj, row0 + r, dom ? P.S_B : P.S_Y, P.L);
         }
-        __syncwarp();
-        // 3. nonzero words: group g = lane + 32q covers coordinates 4g..4g+3, i.e. bits
-        //    4*(lane%8).. of word g/8 = 4q + lane/8
-        uint32_t nibs = 0, word = 0;
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const uint32_t nib = (v[q].x != 0.f ? 1u : 0u) | (v[q].y != 0.f ? 2u : 0u) |
-                                 (v[q].z != 0.f ? 4u : 0u) | (v[q].w != 0.f ? 8u : 0u);
-            nibs |= nib << (4 * q);
-            uint32_t wv = nib << (4 * (lane & 7));
-            wv |= __shfl_xor_sync(kFullMask, wv, 1);
-            wv |= __shfl_xor_sync(kFullMask, wv, 2);
-            wv |= __shfl_xor_sync(kFullMask, wv, 4);
-            const uint32_t t = __shfl_sync(kFullMask, wv, 8 * (lane & 3));
-            if ((lane >> 2) == (uint32_t)q) word = t;
+        if (chunk < nfull) {
+            mbar_wait(bar + st, (it / kStages) & 1u);
+        } else {  // ragged last chunk: plain loads
+            for (uint32_t a = lane; a < kTile; a += 32) cx[a] = base + a < P.d ? x[base + a] : 0.f;
         }
-        my_nnz += __popc(nibs);
-        if (!__any_sync(kFullMask, nibs != 0)) continue;
-        // 4. Bloom filter, lane w = word w of the chunk
+        __syncwarp();
+        // nonzero words: lane w builds word w from its 32 values (eight 16-byte
+        // shared loads, rotated by w so a quarter-warp hits distinct banks)
+        uint32_t word = 0;
         {
+            const float4* cw = reinterpret_cast<const float4*>(cx + 32 * lane);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const uint32_t qq = (q + lane) & 7;
+                const float4 v = cw[qq];
+                const uint32_t nib = (v.x != 0.f ? 1u : 0u) | (v.y != 0.f ? 2u : 0u) |
+                                     (v.z != 0.f ? 4u : 0u) | (v.w != 0.f ? 8u : 0u);
+                word |= nib << (4 * qq);
+            }
+        }
+        const uint32_t nzw = __ballot_sync(kFullMask, word != 0);
+        my_nnz += __popc(word);
+        if (nzw) {  // uniform
+            // Bloom filter, lane w = word w of the chunk
             const uint32_t r = lane >> P.log2nw, w = lane & (P.nw - 1);
             const uint32_t seg = r << P.log2nw;
             for (uint32_t j = 0; j < P.kb; j++) {
@@ -119,30 +200,45 @@ k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ 
                 const uint32_t lo = __shfl_sync(kFullMask, word, seg + sw);
                 const uint32_t hi = __shfl_sync(kFullMask, word, seg + ((sw + 1) & (P.nw - 1)));
                 const uint32_t dst = sh ? (lo >> sh) | (hi << (32 - sh)) : lo;
-                if (dst) atomicOr(bitmap + (uint64_t)mp.x * P.nw + w, dst);
+                if (dst) red_or(bitmap + (uint64_t)mp.x * P.nw + w, dst, pol_keep);
             }
-        }
-        // 5. Count Sketch
-        if (nibs) {
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const uint32_t nib = (nibs >> (4 * q)) & 0xfu;
-                if (!nib) continue;
-                const uint32_t c0 = 4 * (lane + 32 * q);  // coordinate within the chunk
-                const uint32_t r = c0 >> P.log2L, t0 = c0 & (P.L - 1);
-                const float xv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-                for (uint32_t j = 0; j < P.k; j++) {
-                    const uint2 mp = sh_map[r * kk + j];
-                    const float g = map_sign(mp);
-                    const uint64_t rb = (uint64_t)mp.x << P.log2L;
-                    const uint32_t b = map_bias(mp);
-#pragma unroll
-                    for (int e = 0; e < 4; e++)
-                        if (nib & (1u << e)) atomicAdd(counters + rb + ((t0 + e + b) & (P.L - 1)), g * xv[e]);
+            // Count Sketch: sparse chunks — every lane walks its own word's bits;
+            // dense chunks — compact the coordinates, then one nonzero per lane
+            uint32_t maxpop = __popc(word);
+            for (int o = 16; o; o >>= 1) maxpop = max(maxpop, __shfl_xor_sync(kFullMask, maxpop, o));
+            if (maxpop <= 4) {
+                for (uint32_t mm = word; mm; mm &= mm - 1) {
+                    const uint32_t c0 = 32 * lane + (__ffs(mm) - 1);
+                    const float v = cx[c0];
+                    const uint32_t rr = c0 >> P.log2L, t = c0 & (P.L - 1);
+                    for (uint32_t j = 0; j < P.k; j++) {
+                        const uint2 mp = sh_map[rr * kk + j];
+                        red_add(counters + ((uint64_t)mp.x << P.log2L) + ((t + map_bias(mp)) & (P.L - 1)),
+                                map_sign(mp) * v, pol_keep);
+                    }
+                }
+            } else {
+                uint32_t n = 0;
+                for (uint32_t z = nzw; z; z &= z - 1) {
+                    const uint32_t wz = __ffs(z) - 1;
+                    const uint32_t mw = __shfl_sync(kFullMask, word, wz);
+                    if (mw & (1u << lane)) sh_pos[n + __popc(mw & lt)] = (uint16_t)(32 * wz + lane);
+                    n += __popc(mw);
+                }
+                __syncwarp();
+                for (uint32_t a = lane; a < n; a += 32) {
+                    const uint32_t c0 = sh_pos[a];
+                    const float v = cx[c0];
+                    const uint32_t rr = c0 >> P.log2L, t = c0 & (P.L - 1);
+                    for (uint32_t j = 0; j < P.k; j++) {
+                        const uint2 mp = sh_map[rr * kk + j];
+                        red_add(counters + ((uint64_t)mp.x << P.log2L) + ((t + map_bias(mp)) & (P.L - 1)),
+                                map_sign(mp) * v, pol_keep);
+                    }
                 }
             }
         }
-        __syncwarp();  // sh_map is rewritten by the next chunk
+        __syncwarp();  // the stage buffer and the maps are rewritten next
     }
     if (nnz_out) {
         for (int o = 16; o; o >>= 1) my_nnz += __shfl_xor_sync(kFullMask, my_nnz, o);
@@ -153,18 +249,21 @@ k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ 
 void launch_compress_dense(const KParams& P, const float* x, uint32_t* bitmap, float* counters,
                            unsigned long long* nnz_out, cudaStream_t s) {
     const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
-    const size_t smem = (size_t)kCompressWarps * (kTile >> P.log2L) * (P.k + P.kb) * sizeof(uint2);
-    static int per_sm[64] = {0};
+    const uint32_t n_map = (kTile >> P.log2L) * (P.k + P.kb);
+    const size_t smem = kCompressWarps * compress_warp_smem(n_map);
+    static int per_sm[64][6] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && !per_sm[dev]) {
+    const int key = 10 - (int)P.log2L > 5 ? 5 : 10 - (int)P.log2L;
+    if (dev < 64 && !per_sm[dev][key]) {
+        const size_t smax = kCompressWarps * compress_warp_smem(32 * 2 * kMaxK);
+        cudaFuncSetAttribute(k_compress_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
         int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_compress_dense, kCompressThreads,
-                                                      kCompressWarps * 32 * 2 * kMaxK * sizeof(uint2));
-        per_sm[dev] = std::max(1, n);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_compress_dense, kCompressThreads, smem);
+        per_sm[dev][key] = std::max(1, n);
     }
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((nchunks + kCompressWarps - 1) / kCompressWarps,
-                                                         (uint64_t)num_sms() * (dev < 64 ? per_sm[dev] : 2));
+                                                         (uint64_t)num_sms() * (dev < 64 ? per_sm[dev][key] : 2));
     k_compress_dense<<<blocks, kCompressThreads, smem, s>>>(P, x, bitmap, counters, nnz_out);
     count_launch();
 }

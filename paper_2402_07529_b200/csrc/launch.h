@@ -20,6 +20,7 @@ void launch_compress_dense(const KParams& P, const float* x, uint32_t* bitmap, f
                            unsigned long long* nnz_out, cudaStream_t s);
 void launch_compress_coo(const KParams& P, uint64_t nnz, const uint32_t* idx, const float* val,
                          uint32_t* bitmap, float* counters, cudaStream_t s);
+void launch_clear(uint32_t* bitmap, uint64_t n_words, float* counters, uint64_t c, cudaStream_t s);
 void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* const* bitmaps,
                       const float* const* counters, uint32_t* out_bitmap, float* out_counters,
                       cudaStream_t s);

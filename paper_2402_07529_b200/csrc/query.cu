@@ -15,8 +15,8 @@
 //   phase 1  candidate masks of every chunk -> gmask (d/8 bytes), per-chunk counts,
 //            per-CTA totals; also the Count Sketch row-map table for the peel
 //   phase 2  CTA prefix = sum of the totals of the CTAs before it; chunk offsets
-//            (kept for densify); candidates written in ascending order through a
-//            per-warp shared-memory staging buffer (coalesced stores).
+//            (kept for densify); candidates written in ascending order, one
+//            coalesced store per nonzero mask word.
 #include <cooperative_groups.h>
 
 #include "launch.h"
@@ -189,14 +189,36 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
             if (chunk >= nchunks) break;
             const uint32_t msk = __ldcg(gmask + chunk * 32 + lane);
             uint32_t tot;
-            uint32_t pos = warp_excl_scan(__popc(msk), lane, &tot);
-            const uint32_t q0 = (uint32_t)(chunk * kTile + 32 * lane);
-            for (uint32_t mm = msk; mm; mm &= mm - 1) sh_stage[warp][pos++] = q0 + (__ffs(mm) - 1);
-            __syncwarp();
+            const uint32_t pre = warp_excl_scan(__popc(msk), lane, &tot);
             const unsigned long long out0 = tile_base + sh_chunk[cl];
-            for (uint32_t a = lane; a < tot; a += 32)
-                if (out0 + a < cap) out_idx[out0 + a] = sh_stage[warp][a];
-            __syncwarp();
+            const uint32_t chunk_q0 = (uint32_t)(chunk * kTile);
+            const uint32_t nz = __ballot_sync(kFull, msk != 0);
+            uint32_t maxpop = __popc(msk);
+            for (int o = 16; o; o >>= 1) maxpop = max(maxpop, __shfl_xor_sync(kFull, maxpop, o));
+            if ((uint32_t)__popc(nz) <= maxpop) {
+                // few, dense words: one coalesced store per nonzero word (its
+                // candidates are consecutive slots)
+                const uint32_t lt = (1u << lane) - 1u;
+                for (uint32_t z = nz; z; z &= z - 1) {
+                    const uint32_t w = __ffs(z) - 1;
+                    const uint32_t mw = __shfl_sync(kFull, msk, w);
+                    const uint32_t pw = __shfl_sync(kFull, pre, w);
+                    if (mw & (1u << lane)) {
+                        const unsigned long long pos = out0 + pw + __popc(mw & lt);
+                        if (pos < cap) out_idx[pos] = chunk_q0 + 32 * w + lane;
+                    }
+                }
+            } else {
+                // many sparse words: each lane stages its word's candidates in shared
+                // memory (max-popcount iterations), then a coalesced copy
+                uint32_t pos = pre;
+                for (uint32_t mm = msk; mm; mm &= mm - 1)
+                    sh_stage[warp][pos++] = chunk_q0 + 32 * lane + (__ffs(mm) - 1);
+                __syncwarp();
+                for (uint32_t a = lane; a < tot; a += 32)
+                    if (out0 + a < cap) out_idx[out0 + a] = sh_stage[warp][a];
+                __syncwarp();
+            }
         }
         __syncthreads();
     }

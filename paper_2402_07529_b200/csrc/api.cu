@@ -88,11 +88,12 @@ WsLayout ws_layout(const KParams& P, uint64_t cap) {
     W.ctrl = o;      o = align_up(o + sizeof(Ctrl), 256);
     W.tabS = o;      o = align_up(o + nrows * P.k * sizeof(uint2), 256);
     W.gmask = o;     o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);
+    W.woff = o;      o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);
     W.chunk_cnt = o; o = align_up(o + (size_t)W.nchunks * sizeof(uint32_t), 256);
     W.chunk_off = o; o = align_up(o + (size_t)W.nchunks * sizeof(uint32_t), 256);
     W.cta_total = o; o = align_up(o + kMaxQueryCtas * sizeof(uint32_t), 256);
     W.cells = o;     o = align_up(o + P.c * sizeof(CellState), 256);
-    W.claim = o;     o = align_up(o + (std::max<uint64_t>(cap, 1) + 31) / 32 * sizeof(uint32_t), 256);
+    W.claim = o;     o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);  // 1 bit per coordinate
     W.frontier = o;  o = align_up(o + P.c * sizeof(uint2), 256);
     W.total = o;
     return W;
@@ -183,7 +184,7 @@ struct WsView {
     WsLayout W;
     Ctrl* ctrl;
     uint2* tabS;
-    uint32_t *gmask, *chunk_cnt, *chunk_off, *cta_total, *claim;
+    uint32_t *gmask, *woff, *chunk_cnt, *chunk_off, *cta_total, *claim;
     CellState* cells;
     uint2* frontier;
 };
@@ -201,6 +202,7 @@ int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, 
     v->ctrl = reinterpret_cast<Ctrl*>(b + v->W.ctrl);
     v->tabS = reinterpret_cast<uint2*>(b + v->W.tabS);
     v->gmask = reinterpret_cast<uint32_t*>(b + v->W.gmask);
+    v->woff = reinterpret_cast<uint32_t*>(b + v->W.woff);
     v->chunk_cnt = reinterpret_cast<uint32_t*>(b + v->W.chunk_cnt);
     v->chunk_off = reinterpret_cast<uint32_t*>(b + v->W.chunk_off);
     v->cta_total = reinterpret_cast<uint32_t*>(b + v->W.cta_total);
@@ -223,7 +225,7 @@ int sketch_query(const lhc_params* p, const uint32_t* bitmap, void* ws, size_t w
     if (cudaMemsetAsync(v.ctrl, 0, sizeof(Ctrl), s) != cudaSuccess) return check_launch("memset");
     if (cudaMemsetAsync(stats, 0, sizeof(lhc_stats), s) != cudaSuccess) return check_launch("memset");
     cudaError_t e = launch_query(v.P, bitmap, v.tabS, v.gmask, v.chunk_cnt, v.chunk_off, v.cta_total,
-                                 cap_cand, out_idx, v.ctrl, stats, s);
+                                 v.woff, cap_cand, out_idx, v.ctrl, stats, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "query launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_query");
 }
@@ -237,8 +239,9 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
     if (!counters || !stats) return set_error(LHC_EINVAL, "NULL buffer");
     if (!aligned16(counters)) return set_error(LHC_EINVAL, "counters must be 16-byte aligned");
     if (cap_cand && (!out_idx || !out_val || !out_peeled)) return set_error(LHC_EINVAL, "NULL output");
-    cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, cap_cand, v.cells, v.claim,
-                                v.frontier, v.ctrl, out_val, out_peeled, stats, (cudaStream_t)stream);
+    cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, v.gmask, v.woff, cap_cand, v.cells,
+                                v.claim, v.frontier, v.ctrl, out_val, out_peeled, stats,
+                                (cudaStream_t)stream);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_peel");
 }
@@ -251,7 +254,7 @@ int sketch_densify(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t cap_
     if (!out_dense) return set_error(LHC_EINVAL, "NULL out_dense");
     if (!aligned16(out_dense)) return set_error(LHC_EINVAL, "out_dense must be 16-byte aligned");
     if (cap_cand && !out_val) return set_error(LHC_EINVAL, "NULL out_val");
-    launch_densify(v.P, v.gmask, v.chunk_off, cap_cand, out_val, out_dense, (cudaStream_t)stream);
+    launch_densify(v.P, v.gmask, v.woff, cap_cand, out_val, out_dense, (cudaStream_t)stream);
     return check_launch("sketch_densify");
 }
 

@@ -58,10 +58,10 @@ __device__ __forceinline__ uint32_t map_bias(uint2 mp) { return mp.y & 0x7ffffff
 __device__ __forceinline__ float map_sign(uint2 mp) { return (mp.y >> 31) ? -1.0f : 1.0f; }
 
 // Decode state of one Count Sketch cell, 16 bytes so one sector serves both.
-//   key = sum over unpeeled candidates s in the cell of (2^32 + s): the degree is
-//         key >> 32 exactly whenever it is 0 or 1 (then the slot is (uint32)key),
-//         and >= 2 whenever the true degree is >= 2 (degree < 2^31 always holds
-//         since degree <= rows mapped to a cell < 2^27).
+//   key = sum over unpeeled candidates p in the cell of (2^32 + p) (p = coordinate):
+//         the degree is key >> 32 exactly whenever it is 0 or 1 (then the
+//         coordinate is (uint32)key), and >= 2 whenever the true degree is >= 2
+//         (degree < 2^31 always holds since degree <= rows mapped to a cell < 2^27).
 //   R   = residual counter.
 struct __align__(16) CellState {
     unsigned long long key;
@@ -84,6 +84,8 @@ struct Ctrl {
     // round r, t[kCtrlTimes-1] end of rounds; fsize[r] = queue segment of round r
     unsigned long long t[128];
     uint32_t fsize[128];
+    unsigned long long tproc[128];  // per round: latest block finishing its entries
+    unsigned long long tflush[128]; // per round: latest block finishing its appends
 };
 constexpr int kCtrlTimes = 128;
 
@@ -95,7 +97,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // Sub-allocation of the decompress workspace.
 struct WsLayout {
-    size_t tabS, gmask, chunk_cnt, chunk_off, cta_total, cells, claim, frontier, ctrl, total;
+    size_t tabS, gmask, woff, chunk_cnt, chunk_off, cta_total, cells, claim, frontier, ctrl, total;
     uint32_t nchunks;
 };
 

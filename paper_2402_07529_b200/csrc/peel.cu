@@ -5,17 +5,18 @@
 // One cooperative, persistent kernel (grid-wide barriers between phases) so that
 // the whole round loop runs on the device with no host round trips:
 //   init     cell state {key = 0, R = Y}; claim bits cleared
-//   insert   every candidate s adds (2^32 + s) to the key of each of its k cells:
-//            degree and slot sum in one 64-bit reduction
+//   insert   every candidate (coordinate p) adds (2^32 + p) to the key of each of
+//            its k cells: degree and coordinate sum in one 64-bit reduction
 //   F0       every cell of degree one is appended to the frontier queue as the
-//            pair (cell, its only candidate)
-//   rounds   (synchronous, reading R10) for every queue entry (e, s) of the
-//            previous round's segment: claim s (fetch-or of its bit — a candidate can
+//            pair (cell, coordinate of its only candidate)
+//   rounds   (synchronous, reading R10) for every queue entry (e, p) of the
+//            previous round's segment: claim p (fetch-or of its bit — a candidate can
 //            be the only one left in several cells; a stale entry whose candidate
 //            was peeled meanwhile fails the claim), read val = sign * R[e] ("mapped by
 //            only one non-zero parameter"; "X_i can be deduced as
-//            g_j(i) * Y_h_j(i)"), and subtract sign_j * val and (2^32 + s) from all
-//            k cells of s ("deducting Y_h_j(i) by g_j(i) * X_i").  A cell
+//            g_j(i) * Y_h_j(i)"), write it to its slot (the query's per-word slot
+//            offset + rank in the word), and subtract sign_j * val and (2^32 + p)
+//            from the other cells of p ("deducting Y_h_j(i) by g_j(i) * X_i").  A cell
 //            whose degree drops from 2 to 1 is appended for the next round with
 //            its remaining candidate, which is the slot sum left in the key.  A
 //            round consumes only the segment the previous round appended, so the
@@ -32,6 +33,9 @@ namespace cg = cooperative_groups;
 
 namespace lhc {
 
+#ifndef LHC_PEEL_TIMING
+#define LHC_PEEL_TIMING 0
+#endif
 #ifndef LHC_PEEL_THREADS
 #define LHC_PEEL_THREADS 512
 #endif
@@ -45,6 +49,10 @@ __device__ __forceinline__ uint32_t cand_cell(const KParams& P, const uint2* __r
     *neg = mp.y >> 31;
     return (mp.x << P.log2L) + ((t + map_bias(mp)) & (P.L - 1));  // c < 2^32
 }
+
+// queue-buffer entries per thread: a peel appends at most k - 1 cells, an F0
+// pass at most 4
+__host__ __device__ constexpr uint32_t peel_q_per_thread(uint32_t k) { return k - 1 > 4 ? k - 1 : 8; }
 
 // Loads that must stay where they are written (issued before a dependent branch).
 __device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) {
@@ -81,13 +89,13 @@ __device__ __forceinline__ void flush_queue(uint2* sh_q, uint32_t* sh_n, uint32_
 template <int KT>
 __global__ void __launch_bounds__(kPeelThreads)
 k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
-       const uint32_t* __restrict__ cand, uint64_t cap, CellState* cells, uint32_t* claim,
+       const uint32_t* __restrict__ cand, const uint32_t* __restrict__ gmask,
+       const uint32_t* __restrict__ woff, uint64_t cap, CellState* cells, uint32_t* claim,
        uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val, uint8_t* __restrict__ out_peeled,
        lhc_stats* stats) {
     cg::grid_group grid = cg::this_grid();
     constexpr uint32_t NJ = KT ? KT : kMaxK;
-    // a peel appends at most k - 1 cells (the pure cell is never appended):
-    // kPeelThreads * max(1, k - 1) entries of dynamic shared memory
+    // queue buffer: kPeelThreads * peel_q_per_thread(k) entries of dynamic smem
     extern __shared__ uint2 sh_q[];
     __shared__ uint32_t sh_n, sh_base, sh_peeled;
     const uint32_t k = KT ? (uint32_t)KT : P.k;
@@ -107,23 +115,36 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     if (threadIdx.x == 0) { sh_n = 0; sh_peeled = 0; }
     if (timer) ctrl->t[0] = globaltimer();
 
-    // init: cell state {0, Y} (4 cells per thread and pass: 4 loads in flight),
-    // claim bits cleared
-    for (uint64_t e0 = gtid * 4; e0 < P.c; e0 += gstride * 4) {  // c is a multiple of 32
-        const float4 y = __ldcs(reinterpret_cast<const float4*>(counters + e0));
-        CellState st;
-        st.key = 0ull;
-        st.pad = 0u;
-        st.R = y.x; cells[e0] = st;
-        st.R = y.y; cells[e0 + 1] = st;
-        st.R = y.z; cells[e0 + 2] = st;
-        st.R = y.w; cells[e0 + 3] = st;
+    // init: cell state {0, Y} (coalesced: one 16-byte cell per lane, 4 passes
+    // unrolled so 4 loads are in flight), claim bits cleared
+    {
+        uint64_t e = gtid;
+        for (; e + 3 * gstride < P.c; e += 4 * gstride) {
+            float y[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) y[u] = __ldcs(counters + e + u * gstride);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                CellState st;
+                st.key = 0ull;
+                st.R = y[u];
+                st.pad = 0u;
+                cells[e + u * gstride] = st;
+            }
+        }
+        for (; e < P.c; e += gstride) {
+            CellState st;
+            st.key = 0ull;
+            st.R = __ldcs(counters + e);
+            st.pad = 0u;
+            cells[e] = st;
+        }
     }
-    for (uint64_t w = gtid; w < (n_c + 31) / 32; w += gstride) claim[w] = 0u;
+    for (uint64_t w = gtid; w < ((uint64_t)P.d + 31) / 32; w += gstride) claim[w] = 0u;
     grid.sync();
     if (timer) ctrl->t[1] = globaltimer();
 
-    // insert: degree and slot sum of every cell
+    // insert: degree and coordinate sum of every cell
     for (uint64_t s = gtid; s < n_c; s += gstride) {
         const uint32_t p = __ldg(cand + s);
 #pragma unroll
@@ -131,20 +152,33 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
             if (!KT && j >= k) break;
             uint32_t neg;
             const uint32_t e = cand_cell(P, tabS, p, j, &neg);
-            atomicAdd(&cells[e].key, (1ull << 32) + s);
+            atomicAdd(&cells[e].key, (1ull << 32) + p);
         }
     }
     grid.sync();
     if (timer) ctrl->t[2] = globaltimer();
 
     // F0 ("round 0"): cells of degree one with their candidate, through rc[0]
-    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < P.c; base += gstride) {
-        const uint64_t e = base + threadIdx.x;
-        if (e < P.c) {
-            const unsigned long long key = __ldcg(&cells[e].key);
-            if ((key >> 32) == 1ull) sh_q[atomicAdd(&sh_n, 1u)] = make_uint2((uint32_t)e, (uint32_t)key);
+    {
+        // four cells per thread and pass (four loads in flight); one global
+        // reservation per buffer-full, not per pass
+        const uint32_t qcap = kPeelThreads * peel_q_per_thread(k);  // entries of sh_q
+        for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < P.c; base += 4 * gstride) {
+            unsigned long long key[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint64_t e = base + u * gstride + threadIdx.x;
+                key[u] = e < P.c ? __ldcg(&cells[e].key) : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if ((key[u] >> 32) == 1ull)
+                    sh_q[atomicAdd(&sh_n, 1u)] =
+                        make_uint2((uint32_t)(base + u * gstride + threadIdx.x), (uint32_t)key[u]);
+            __syncthreads();
+            if (sh_n + 4 * kPeelThreads > qcap || base + 4 * gstride >= P.c)
+                flush_queue(sh_q, &sh_n, &sh_base, frontier, 0u, &ctrl->rc[0]);
         }
-        flush_queue(sh_q, &sh_n, &sh_base, frontier, 0u, &ctrl->rc[0]);
     }
     grid.sync();
     if (timer) ctrl->t[3] = globaltimer();
@@ -166,15 +200,15 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
             const uint64_t f = base + threadIdx.x;
             if (f < f_end) {
                 const uint2 ent = frontier[f];
-                const uint32_t e = ent.x, s = ent.y;
-                // issued back to back (volatile loads are not sunk into the branch):
-                // the candidate, the pure cell's residual and the claim (fetch-or of the
-                // candidate's bit: a candidate can be the only one left in several
-                // cells; a stale entry finds its bit already set), then the row maps
-                const uint32_t p = ld_nc_u32(cand + s);
+                const uint32_t e = ent.x, p = ent.y;
+                // issued back to back (volatile loads are not sunk into the branch): the
+                // claim (fetch-or of the candidate's bit: a candidate can be the only one
+                // left in several cells; a stale entry finds its bit already set), the
+                // pure cell's residual, the row maps and the slot of p (the query's
+                // per-word slot offset and mask)
+                const uint32_t bit = 1u << (p & 31);
+                const uint32_t old = atomicOr(claim + (p >> 5), bit);
                 const float Re = ld_cg_f32(&cells[e].R);
-                const uint32_t bit = 1u << (s & 31);
-                const uint32_t old = atomicOr(claim + (s >> 5), bit);
                 const uint2* row = tabS + (uint64_t)(p >> P.log2L) * k;
                 uint2 mp[NJ];
 #pragma unroll
@@ -182,6 +216,8 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                     if (!KT && j >= k) break;
                     mp[j] = ld_nc_u2(row + j);
                 }
+                const uint32_t wo = ld_nc_u32(woff + (p >> 5));
+                const uint32_t wm = ld_nc_u32(gmask + (p >> 5));
                 if (!(old & bit)) {
                     const uint32_t t = p & (P.L - 1);
                     uint32_t ev[NJ];
@@ -193,18 +229,18 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                         if (ev[j] == e) ge = map_sign(mp[j]);
                     }
                     const float val = ge * Re;
-                    out_val[s] = val;
+                    out_val[wo + __popc(wm & (bit - 1u))] = val;
                     atomicAdd(&sh_peeled, 1u);
                     // all reductions first (independent), then the queue appends
                     unsigned long long rest[NJ];
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
-                        // the pure cell held only s: nothing reads its state again
+                        // the pure cell held only p: nothing reads its state again
                         if (ev[j] == e) continue;
                         atomicAdd(&cells[ev[j]].R, -map_sign(mp[j]) * val);
-                        rest[j] = atomicAdd(&cells[ev[j]].key, 0ull - ((1ull << 32) + s)) -
-                                  ((1ull << 32) + s);
+                        rest[j] = atomicAdd(&cells[ev[j]].key, 0ull - ((1ull << 32) + p)) -
+                                  ((1ull << 32) + p);
                     }
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
@@ -214,7 +250,11 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                     }
                 }
             }
+            if (LHC_PEEL_TIMING && threadIdx.x == 0 && r < kCtrlTimes)
+                atomicMax(&ctrl->tproc[r], globaltimer());
             flush_queue(sh_q, &sh_n, &sh_base, frontier, f_end, rc);
+            if (LHC_PEEL_TIMING && threadIdx.x == 0 && r < kCtrlTimes)
+                atomicMax(&ctrl->tflush[r], globaltimer());
         }
         if (threadIdx.x == 0 && sh_peeled) {
             atomicAdd(rc, (unsigned long long)sh_peeled << 32);
@@ -232,10 +272,10 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
 
     // finalize: median estimate of unpeeled candidates
     for (uint64_t s = gtid; s < n_c; s += gstride) {
-        const bool pe = (__ldcg(claim + (s >> 5)) >> (s & 31)) & 1u;
+        const uint32_t p = __ldg(cand + s);
+        const bool pe = (__ldcg(claim + (p >> 5)) >> (p & 31)) & 1u;
         out_peeled[s] = pe ? 1 : 0;
         if (!pe) {
-            const uint32_t p = __ldg(cand + s);
             float v[NJ];
             for (uint32_t j = 0; j < k; j++) {
                 uint32_t neg;
@@ -259,7 +299,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     }
 }
 
-static size_t peel_smem(uint32_t k) { return (size_t)kPeelThreads * (k > 1 ? k - 1 : 1) * sizeof(uint2); }
+static size_t peel_smem(uint32_t k) { return (size_t)kPeelThreads * peel_q_per_thread(k) * sizeof(uint2); }
 
 template <int KT>
 static int peel_grid(int dev, uint32_t k) {
@@ -274,15 +314,17 @@ static int peel_grid(int dev, uint32_t k) {
 }
 
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
-                        const uint32_t* cand, uint64_t cap, CellState* cells, uint32_t* claim,
-                        uint2* frontier, Ctrl* ctrl, float* out_val, uint8_t* out_peeled,
-                        lhc_stats* stats, cudaStream_t s) {
+                        const uint32_t* cand, const uint32_t* gmask, const uint32_t* woff,
+                        uint64_t cap, CellState* cells, uint32_t* claim, uint2* frontier,
+                        Ctrl* ctrl, float* out_val, uint8_t* out_peeled, lhc_stats* stats,
+                        cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     KParams Pc = P;
     void* args[] = {(void*)&Pc,    (void*)&counters, (void*)&tabS,     (void*)&cand,
-                    (void*)&cap,   (void*)&cells,    (void*)&claim,    (void*)&frontier,
-                    (void*)&ctrl,  (void*)&out_val,  (void*)&out_peeled, (void*)&stats};
+                    (void*)&gmask, (void*)&woff,     (void*)&cap,      (void*)&cells,
+                    (void*)&claim, (void*)&frontier, (void*)&ctrl,     (void*)&out_val,
+                    (void*)&out_peeled, (void*)&stats};
     cudaError_t err;
     if (P.k == 3)
         err = cudaLaunchCooperativeKernel((const void*)k_peel<3>, dim3(peel_grid<3>(dev, 3)),

@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--gamma", type=float, default=1.30)
     ap.add_argument("--law", default="gauss")
+    ap.add_argument("--index", choices=["bloom", "bitmap", "auto"], default="bloom",
+                    help="Bloom filter (default), exact bitmap (P:L188), or the smaller of the two")
     ap.add_argument("--fuse-local", action="store_true",
                     help="compress a rank's workers straight into one sketch (no per-worker sketches)")
     ap.add_argument("--comm", choices=["p2p", "nccl"], default="p2p")
@@ -220,8 +222,13 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     lhc.lib()
 
-    sz = lhc.size_workload(wl.d, wl.density, wl.workers, gamma=args.gamma)
-    p = lhc.params(wl.d, sz.m, sz.c, 3, 0, 1024, SEED)
+    from paper_2402_07529_b200.sizing import INDEX_BITMAP, smaller_index
+
+    kb = {"bloom": 0, "bitmap": INDEX_BITMAP}.get(args.index)
+    if kb is None:
+        kb = smaller_index(wl.d, wl.density, wl.workers, gamma=args.gamma)
+    sz = lhc.size_workload(wl.d, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb)
+    p = lhc.params(wl.d, sz.m, sz.c, 3, kb, 1024, SEED)
     cap = min(wl.d, int(sz.n_cand_expected * 1.25) + 4096)
     my_workers = lhc.pipeline.owned_workers(wl.workers, rank, world)
 
@@ -450,6 +457,7 @@ def main():
             "config": {"workload": wl.name, "d": wl.d, "density": wl.density,
                        "workers": wl.workers, "structure": wl.structure, "law": wl.law,
                        "k": 3, "L": 1024, "m": int(p.m), "c": int(p.c), "gamma": args.gamma,
+                       "index": "bitmap" if kb == INDEX_BITMAP else "bloom",
                        "sketch_bytes": int(p.m) // 8 + 4 * int(p.c),
                        "per_worker_sketches": run.per_worker,
                        "comm": ("p2p" if comm is not None else "nccl") if world > 1 else "none",

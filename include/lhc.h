@@ -57,10 +57,15 @@ typedef struct lhc_params {
     uint64_t m;        /* Bloom-filter bits, multiple of k_bloom*L, m/L < 2^32     */
     uint64_t c;        /* Count Sketch cells, multiple of k*L, c < 2^32 (size of Y) */
     uint32_t k;        /* Count Sketch hashes, 1..8 (paper: 3)                      */
-    uint32_t k_bloom;  /* Bloom probes, 0..8; 0 means k (paper: log 1/eps)         */
+    uint32_t k_bloom;  /* Bloom probes, 0..8; 0 means k (paper: log 1/eps);        *
+                        * LHC_INDEX_BITMAP: the exact bitmap index of §3.2 (one bit *
+                        * per parameter, bit p = coordinate p; requires m = ceil(d/L)*L)    */
     uint32_t L;        /* batch width, power of two in [32, 1024] (paper: c=1024)  */
     uint64_t seed;     /* hash seed; every rank must use the same one                       */
 } lhc_params;
+
+/* k_bloom value selecting the exact bitmap index instead of a Bloom filter. */
+#define LHC_INDEX_BITMAP 255u
 
 /* Device-resident decode statistics (§4.1.1 metrics). */
 typedef struct lhc_stats {

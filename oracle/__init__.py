@@ -113,7 +113,12 @@ def params(d, m, c, k=3, k_bloom=0, L=1024, seed=0) -> Params:
     return Params(int(d), int(m), int(c), int(k), int(k_bloom), int(L), int(seed) & (2**64 - 1))
 
 
+INDEX_BITMAP = 255  # k_bloom value of the exact bitmap index
+
+
 def k_bloom_of(p: Params) -> int:
+    if p.k_bloom == INDEX_BITMAP:
+        return 1
     return p.k_bloom or p.k
 
 

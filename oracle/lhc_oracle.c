@@ -67,7 +67,16 @@ typedef struct {
 
 enum { ORA_OK = 0, ORA_EINVAL = 1 };
 
-static uint32_t kb_of(const ora_params* p) { return p->k_bloom ? p->k_bloom : p->k; }
+/* k_bloom value selecting the exact bitmap index of §3.2 ("allocating one
+ * bit per parameter - for each bit, true indicates non-zero, while false
+ * indicates zero") instead of a Bloom filter: bit p is coordinate p. */
+#define ORA_INDEX_BITMAP 255u
+
+static uint32_t kb_of(const ora_params* p)
+{
+    if (p->k_bloom == ORA_INDEX_BITMAP) return 1;
+    return p->k_bloom ? p->k_bloom : p->k;
+}
 
 /* ---------------------------------------------------------------------------
  * Hashing (reading R1; the paper only says "hashed to three signals ... and
@@ -101,6 +110,12 @@ uint64_t ora_hash(uint64_t seed, uint32_t dom, uint32_t j, uint64_t i)
 void ora_row_map(const ora_params* p, uint32_t dom, uint32_t j, uint64_t i,
                  uint64_t* row, uint32_t* bias, int* sign)
 {
+    if (dom == 1 && p->k_bloom == ORA_INDEX_BITMAP) { /* exact bitmap: row i, no rotation */
+        *row = i;
+        *bias = 0;
+        *sign = +1;
+        return;
+    }
     uint64_t S = dom == 0 ? p->c / ((uint64_t)p->k * p->L)
                           : p->m / ((uint64_t)kb_of(p) * p->L);
     uint64_t H = ora_hash(p->seed, dom, j, i);
@@ -138,7 +153,9 @@ static void bit_set(uint32_t* B, uint64_t b) { B[b >> 5] |= 1u << (b & 31); }
 
 int ora_validate(const ora_params* p)
 {
-    if (!p || p->d == 0 || p->k == 0 || p->k > 8 || p->k_bloom > 8)
+    if (!p || p->d == 0 || p->k == 0 || p->k > 8) return ORA_EINVAL;
+    if (p->k_bloom > 8 && p->k_bloom != ORA_INDEX_BITMAP) return ORA_EINVAL;
+    if (p->k_bloom == ORA_INDEX_BITMAP && p->m != ((uint64_t)p->d + p->L - 1) / p->L * p->L)
         return ORA_EINVAL;
     if (p->L < 32 || p->L > 1024 || (p->L & (p->L - 1))) return ORA_EINVAL;
     uint32_t kb = kb_of(p);

@@ -51,10 +51,15 @@ int validate(const lhc_params* p) {
     if (!p) return set_error(LHC_EINVAL, "params is NULL");
     if (p->d == 0) return set_error(LHC_EINVAL, "d must be >= 1");
     if (p->k == 0 || p->k > (uint32_t)kMaxK) return set_error(LHC_EINVAL, "k must be in [1, 8]");
-    if (p->k_bloom > (uint32_t)kMaxK) return set_error(LHC_EINVAL, "k_bloom must be in [0, 8]");
     if (p->L < 32 || p->L > 1024 || (p->L & (p->L - 1)))
         return set_error(LHC_EINVAL, "L must be a power of two in [32, 1024]");
-    const uint32_t kb = p->k_bloom ? p->k_bloom : p->k;
+    if (p->k_bloom == LHC_INDEX_BITMAP) {
+        const uint64_t rows = ((uint64_t)p->d + p->L - 1) / p->L;
+        if (p->m != rows * p->L) return set_error(LHC_EINVAL, "exact bitmap index needs m = ceil(d/L)*L");
+    } else if (p->k_bloom > (uint32_t)kMaxK) {
+        return set_error(LHC_EINVAL, "k_bloom must be in [0, 8] or LHC_INDEX_BITMAP");
+    }
+    const uint32_t kb = p->k_bloom == LHC_INDEX_BITMAP ? 1u : p->k_bloom ? p->k_bloom : p->k;
     if (p->c == 0 || p->c % ((uint64_t)p->k * p->L)) return set_error(LHC_EINVAL, "c must be a positive multiple of k*L");
     if (p->m == 0 || p->m % ((uint64_t)kb * p->L)) return set_error(LHC_EINVAL, "m must be a positive multiple of k_bloom*L");
     if (p->c >= (1ull << 32)) return set_error(LHC_EINVAL, "c must be < 2^32");
@@ -69,7 +74,8 @@ KParams kparams(const lhc_params* p) {
     K.m = p->m;
     K.d = p->d;
     K.k = p->k;
-    K.kb = p->k_bloom ? p->k_bloom : p->k;
+    K.exact = p->k_bloom == LHC_INDEX_BITMAP ? 1u : 0u;
+    K.kb = K.exact ? 1u : p->k_bloom ? p->k_bloom : p->k;
     K.L = p->L;
     K.log2L = ilog2(p->L);
     K.nw = p->L / 32;

@@ -10,13 +10,12 @@ namespace lhc {
 // ---------------------------------------------------------------------------
 __global__ void k_hash_rows(KParams P, uint32_t dom, uint64_t n_rows, uint2* __restrict__ out) {
     const uint32_t kk = dom == 0 ? P.k : P.kb;
-    const uint32_t S = dom == 0 ? P.S_Y : P.S_B;
     const uint64_t n = n_rows * kk;
     for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
          q += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t i = q / kk;
         uint32_t j = (uint32_t)(q - i * kk);
-        out[q] = row_map(P.seed, dom, j, i, S, P.L);
+        out[q] = dom_map(P, dom, j, i);
     }
 }
 
@@ -165,7 +164,7 @@ k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ 
         for (uint32_t a = lane; a < n_map; a += 32) {
             const uint32_t r = a / kk, jj = a - r * kk;
             const uint32_t dom = jj < P.k ? 0u : 1u;
-            sh_map[a] = row_map(P.seed, dom, dom ? jj - P.k : jj, row0 + r, dom ? P.S_B : P.S_Y, P.L);
+            sh_map[a] = dom_map(P, dom, dom ? jj - P.k : jj, row0 + r);
         }
         if (chunk < nfull) {
             mbar_wait(bar + st, (it / kStages) & 1u);
@@ -285,7 +284,7 @@ k_compress_coo(KParams P, uint64_t nnz, const uint32_t* __restrict__ idx,
         const uint64_t i = p >> P.log2L;
         const uint32_t t = p & (P.L - 1);
         for (uint32_t j = 0; j < P.kb; j++) {
-            const uint2 mp = row_map(P.seed, 1, j, i, P.S_B, P.L);
+            const uint2 mp = dom_map(P, 1, j, i);
             const uint64_t b = ((uint64_t)mp.x << P.log2L) + ((t + map_bias(mp)) & (P.L - 1));
             const uint64_t word = b >> 5;
             uint32_t bits = live ? (1u << (b & 31)) : 0u;
@@ -297,7 +296,7 @@ k_compress_coo(KParams P, uint64_t nnz, const uint32_t* __restrict__ idx,
         }
         if (live) {
             for (uint32_t j = 0; j < P.k; j++) {
-                const uint2 mp = row_map(P.seed, 0, j, i, P.S_Y, P.L);
+                const uint2 mp = dom_map(P, 0, j, i);
                 const uint64_t e = ((uint64_t)mp.x << P.log2L) + ((t + map_bias(mp)) & (P.L - 1));
                 atomicAdd(counters + e, map_sign(mp) * xv);
             }

@@ -25,6 +25,7 @@ struct KParams {
     uint32_t S_Y;      // rows per sketch partition
     uint32_t S_B;      // rows per bloom partition
     uint32_t nrows;    // ceil(d / L)
+    uint32_t exact;    // 1: the index is the exact bitmap, bit p <-> coordinate p
 };
 
 // ---------------------------------------------------------------------------
@@ -52,6 +53,15 @@ __host__ __device__ __forceinline__ uint2 row_map(uint64_t seed, uint32_t dom, u
     uint32_t row = j * S + (uint32_t)(((H >> 32) * (uint64_t)S) >> 32);
     uint32_t y = (uint32_t)(H & (uint64_t)(L - 1)) | ((uint32_t)((H >> 16) & 1u) << 31);
     return make_uint2(row, y);
+}
+
+// Row map of domain dom (0 = Count Sketch, 1 = index) for input row i under probe j.
+// With the exact bitmap index ("one bit per parameter") the index row of
+// input row i is row i itself, unrotated.
+__host__ __device__ __forceinline__ uint2 dom_map(const KParams& P, uint32_t dom, uint32_t j,
+                                                  uint64_t i) {
+    if (dom == 1 && P.exact) return make_uint2((uint32_t)i, 0u);
+    return row_map(P.seed, dom, j, i, dom ? P.S_B : P.S_Y, P.L);
 }
 
 __device__ __forceinline__ uint32_t map_bias(uint2 mp) { return mp.y & 0x7fffffffu; }

@@ -63,7 +63,7 @@ __device__ __forceinline__ void query_chunks(const KParams& P, const uint32_t* _
         // row maps: lane seg + j hashes probe j of the row when the row spans >= kb lanes
         uint2 mine = make_uint2(0u, 0u);
         if (P.nw >= kb) {
-            if (live && w < kb) mine = row_map(P.seed, 1, w, i, P.S_B, P.L);
+            if (live && w < kb) mine = dom_map(P, 1, w, i);
         }
 #pragma unroll
         for (uint32_t j = 0; j < NJ; j++) {
@@ -73,7 +73,7 @@ __device__ __forceinline__ void query_chunks(const KParams& P, const uint32_t* _
                 mp.x = __shfl_sync(kFull, mine.x, seg + j);
                 mp.y = __shfl_sync(kFull, mine.y, seg + j);
             } else {
-                mp = live ? row_map(P.seed, 1, j, i, P.S_B, P.L) : make_uint2(0u, 0u);
+                mp = live ? dom_map(P, 1, j, i) : make_uint2(0u, 0u);
             }
             bias[it][j] = map_bias(mp);
             // every lane of a live row loads its word, even past d: the rotation
@@ -126,7 +126,7 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
         for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
              q += (uint64_t)gridDim.x * blockDim.x) {
             const uint64_t i = q / P.k;
-            tabS[q] = row_map(P.seed, 0, (uint32_t)(q - i * P.k), i, P.S_Y, P.L);
+            tabS[q] = dom_map(P, 0, (uint32_t)(q - i * P.k), i);
         }
     }
 

@@ -65,9 +65,20 @@ def _round_up(x: float, q: int) -> int:
     return int(math.ceil(x / q)) * q
 
 
+INDEX_BITMAP = 255  # k_bloom value of the exact bitmap index (include/lhc.h)
+
+
 def size_for(d: int, n: float, k: int = 3, k_bloom: int = 0, L: int = 1024,
              gamma: float = GAMMA_DEFAULT) -> Sizing:
-    """(m, c) minimising m + 32c for an expected aggregate support of n coordinates."""
+    """(m, c) minimising m + 32c for an expected aggregate support of n coordinates.
+
+    k_bloom = INDEX_BITMAP selects the exact bitmap index of §3.2: m is one
+    bit per coordinate (rounded up to whole rows), no false positives, c = gamma n."""
+    if k_bloom == INDEX_BITMAP:
+        n = max(float(n), 1.0)
+        m = (d + L - 1) // L * L
+        c = max(k * L, _round_up(gamma * n, k * L))
+        return Sizing(d, m, c, k, INDEX_BITMAP, L, n, 0.0, n, gamma)
     kb = k_bloom or k
     qm, qc = kb * L, k * L
     n = max(float(n), 1.0)
@@ -88,6 +99,16 @@ def size_for(d: int, n: float, k: int = 3, k_bloom: int = 0, L: int = 1024,
 
 def size_workload(d: int, density: float, workers: int, **kw) -> Sizing:
     return size_for(d, union_support(d, density, workers), **kw)
+
+
+def smaller_index(d: int, density: float, workers: int, **kw) -> int:
+    """The index kind with the smaller sketch for this workload: 0 (Bloom filter
+    with k probes) or INDEX_BITMAP (the paper's footnote P:L160: the Bloom filter is
+    "only theoretically necessary when the sparsity is extremely high")."""
+    bloom = size_workload(d, density, workers, **kw)
+    exact = size_workload(d, density, workers, k_bloom=INDEX_BITMAP,
+                          **{k: v for k, v in kw.items() if k != "k_bloom"})
+    return INDEX_BITMAP if exact.sketch_bytes < bloom.sketch_bytes else 0
 
 
 # ---- §3.3 theory (P:L213-250) ------------------------------------------------

@@ -278,10 +278,32 @@ def test_determinism_of_indices_and_flags(lhc):
     assert outs[0][3] == outs[1][3]
 
 
+# ------------------------------------------------ exact bitmap index (NEXT-1) --
+
+@pytest.mark.parametrize("d,nnz,W,L", [(10_000, 100, 2, 1024), (1_000_003, 10_000, 3, 1024),
+                                      (777_777, 30_000, 4, 32)])
+@pytest.mark.parametrize("law", ["dyadic", "gauss"])
+def test_pipeline_exact_bitmap(lhc, ora, d, nnz, W, L, law):
+    from paper_2402_07529_b200.sizing import INDEX_BITMAP
+
+    s = lhc.size_workload(d, nnz / d, W, L=L, k_bloom=INDEX_BITMAP)
+    p = gpu_params(lhc, d, s.m, s.c, kb=INDEX_BITMAP, L=L, seed=0xB17 + d)
+    op = ora_params(ora, p)
+    xs = make_workers(d, nnz, W, 91 + d % 7, law)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(op, xs)
+    assert np.array_equal(U(run.sketch.bitmap), B)
+    assert_values(F(run.sketch.counters), Y, law == "dyadic")
+    compare_decode(ora, dec, ref, law == "dyadic")
+
+
 # ------------------------------------------------- BASELINE.json full sizes --
 
 FULL = [
     ("ncf", {}),
+    ("ncf", {"index": "bitmap"}),
     ("lstm", {}),
     ("bert", {"density": 0.01}),
     ("bert", {"density": 0.10}),
@@ -290,13 +312,18 @@ FULL = [
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name,over", FULL, ids=[f"{n}-{o.get('density', '')}" for n, o in FULL])
+@pytest.mark.parametrize("name,over", FULL,
+                         ids=[f"{n}-{o.get('density', '')}{o.get('index', '')}" for n, o in FULL])
 def test_full_size_configs(lhc, ora, name, over):
     """The bench's launch configuration (per-worker sketches aggregated on one GPU,
     one decode) at the configs' full sizes, compared in full with the oracle."""
+    from paper_2402_07529_b200.sizing import INDEX_BITMAP
+
+    over = dict(over)
+    kb = INDEX_BITMAP if over.pop("index", "bloom") == "bitmap" else 0
     wl = config(name, **over)
-    s = lhc.size_workload(wl.d, wl.density, wl.workers)
-    p = gpu_params(lhc, wl.d, s.m, s.c, seed=0x1DC0DE)
+    s = lhc.size_workload(wl.d, wl.density, wl.workers, k_bloom=kb)
+    p = gpu_params(lhc, wl.d, s.m, s.c, kb=kb, seed=0x1DC0DE)
     op = ora_params(ora, p)
     xs = [wl.dense(w) for w in range(wl.workers)]
     run = lhc.LosslessAllReduce(p, cap_cand=int(s.n_cand_expected * 1.5) + 1024,

@@ -467,3 +467,40 @@ def test_all_zero_gradient(ora):
     B, Y, dec = ora.pipeline(p, [np.zeros(p.d, np.float32)])
     assert dec.stats.n_cand == 0 and dec.stats.success and dec.stats.rounds == 0
     assert not dec.dense.any()
+
+
+# ------------------------------------------------ exact bitmap index (NEXT-1) --
+
+@pytest.mark.parametrize("L", [32, 1024])
+def test_exact_bitmap_is_the_support(ora, L):
+    # "allocating one bit per parameter - for each bit, true indicates
+    # non-zero, while false indicates zero"; OR-homomorphic across workers.
+    d = 50_003
+    m = (d + L - 1) // L * L
+    p = P(ora, d, m, 3 * L * 8, kb=ora.INDEX_BITMAP, L=L, seed=9)
+    assert ora.validate(p)
+    assert not ora.validate(P(ora, d, m + L, 3 * L * 8, kb=ora.INDEX_BITMAP, L=L))
+    xs = _workers(d, 700, 3, 70)
+    B = None
+    Y = None
+    for x in xs:
+        B, Y = ora.compress_dense(p, x, B, Y)
+    support = np.zeros(m, bool)
+    for x in xs:
+        support[:d] |= x != 0
+    ref = np.packbits(support, bitorder="little").view(np.uint32)
+    assert np.array_equal(B, ref)
+    assert np.array_equal(ora.query(p, B), np.flatnonzero(support).astype(np.uint32))
+
+
+def test_exact_bitmap_lossless(ora):
+    from paper_2402_07529_b200.sizing import INDEX_BITMAP, size_for, union_support
+
+    d, W, L = 300_001, 4, 1024
+    s = size_for(d, union_support(d, 2000 / d, W), k_bloom=INDEX_BITMAP, L=L, gamma=1.4)
+    p = P(ora, d, s.m, s.c, kb=ora.INDEX_BITMAP, L=L, seed=5)
+    xs = _workers(d, 2000, W, 800)
+    _, _, dec = ora.pipeline(p, xs)
+    truth = np.sum(np.stack(xs).astype(np.float64), axis=0)
+    assert dec.stats.success and np.array_equal(dec.dense, truth)
+    assert dec.stats.n_cand == int((np.stack(xs) != 0).any(axis=0).sum())  # no false positives

@@ -54,6 +54,7 @@ def parse():
                     help="compress a rank's workers straight into one sketch (no per-worker sketches)")
     ap.add_argument("--comm", choices=["p2p", "nccl"], default="p2p")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     ap.add_argument("--phases", action="store_true", help="also print per-phase times (stderr)")
@@ -324,24 +325,15 @@ def main():
     trace('timed')
     # ---- timed region: K steps, per-step events, L2 flushed between steps ----
     clocks = ClockSampler(local_rank)
-    clocks.start()
-    time.sleep(0.3)
-    per_step = []
     phase = {"compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "query": 0.0, "peel": 0.0,
              "densify": 0.0}
     compress_launch_ms = []
     launches = [0]
-    barrier()
-    for _ in range(args.steps):
-        flush.zero_()
-        ev = []
-        step(ev, launches)
-        per_step.append(ev)
-    barrier()
-    clocks.stop()
     total_ms = 0.0
-    for ev in per_step:
-        t = dict()
+
+    def collect(ev):
+        """Fold one step's (name, event) marks into the totals."""
+        nonlocal total_ms
         st = ev[0][1]
         total_ms += st.elapsed_time(ev[-1][1])
         prev = st
@@ -353,7 +345,57 @@ def main():
             elif name in phase:
                 phase[name] += dt
             prev = e
-        del t
+
+    graph = None
+    if not args.no_graph:
+        # the whole step as one CUDA graph: every kernel replayed without host launch
+        # overhead (the cooperative kernels and the NVLink all-reduce are capturable;
+        # the all-reduce keeps its barrier epoch on the device)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        cap_launches = [0]
+        with torch.cuda.graph(graph, stream=side):
+            stream = torch.cuda.current_stream()
+            step(None, cap_launches)
+        stream = torch.cuda.current_stream()
+        stream.wait_stream(side)
+        for _ in range(2):
+            graph.replay()
+        barrier()
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    # (1) headline: K steps, device time per step from events around each step
+    step_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            step(None, launches)
+        e1.record(stream)
+        step_ms.append((e0, e1))
+    barrier()
+    if graph is not None:
+        launches[0] = cap_launches[0] * args.steps
+    # (2) per-kernel breakdown: K instrumented steps launched from the host, CUDA
+    #     events between the kernels on the launching stream
+    per_step = []
+    for _ in range(args.steps):
+        flush.zero_()
+        ev = []
+        step(ev, None)
+        per_step.append(ev)
+    torch.cuda.synchronize()
+    for ev in per_step:
+        collect(ev)
+    total_ms = sum(a.elapsed_time(b) for a, b in step_ms)
+    barrier()
+    clocks.stop()
     ms = total_ms / args.steps
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -461,7 +503,10 @@ def main():
                        "sketch_bytes": int(p.m) // 8 + 4 * int(p.c),
                        "per_worker_sketches": run.per_worker,
                        "comm": ("p2p" if comm is not None else "nccl") if world > 1 else "none",
-                       "l2": "flushed (256 MB write) between timed steps, outside the events"},
+                       "l2": "flushed (256 MB write) between timed steps, outside the events",
+                       "cuda_graph": graph is not None,
+                       "kernel_timing": "CUDA events between kernels in a second K-step pass "
+                                        "launched from the host (same inputs, L2 flushed)"},
             "roofline": roofline,
             "kernels": kernels,
             "cpu_baseline": cpu,

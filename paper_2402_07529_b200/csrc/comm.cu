@@ -13,7 +13,8 @@
 //   barrier C      nobody reads our buffer any more (the caller may reuse it)
 // Barriers: block 0 publishes the epoch to every peer's signal slot with a
 // system-scope release store and spins on its own slots with acquire loads; the
-// rest of the grid waits at a grid-wide barrier.  Bytes per rank and direction:
+// rest of the grid waits at a grid-wide barrier.  The epoch counter is kept on
+// the device, so the call is CUDA-graph capturable and replayable.  Bytes per rank and direction:
 // 2(G-1)/G * S.
 #include <cooperative_groups.h>
 #include <cuda.h>
@@ -36,7 +37,6 @@ struct ArArgs {
     uint4* my_b;
     float4* my_y;
     uint64_t nb4, nc4;          // 16-byte units per region
-    uint32_t epoch;
     int rank, world;
 };
 
@@ -69,12 +69,22 @@ __device__ __forceinline__ void slice(uint64_t n, int q, int world, uint64_t* lo
     *hi = n * (q + 1) / world;
 }
 
+// The barrier epoch lives in the rank's own signal area (slot kEpochSlot) and is
+// advanced by the kernel itself, so a captured CUDA graph can be replayed.
+constexpr int kEpochSlot = 32;
+
 __global__ void __launch_bounds__(256) k_allreduce(ArArgs A) {
     cg::grid_group grid = cg::this_grid();
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    __shared__ uint32_t sh_epoch;
+    if (blockIdx.x == 0) {
+        if (threadIdx.x == 0) sh_epoch = *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot);
+        __syncthreads();
+    }
+    const uint32_t epoch = blockIdx.x == 0 ? sh_epoch : 0u;
 
-    if (blockIdx.x == 0) xrank_barrier(A, A.epoch + 1);
+    if (blockIdx.x == 0) xrank_barrier(A, epoch + 1);
     grid.sync();
 
     // reduce-scatter of my slice
@@ -98,7 +108,7 @@ __global__ void __launch_bounds__(256) k_allreduce(ArArgs A) {
         A.my_y[u] = acc;
     }
     grid.sync();
-    if (blockIdx.x == 0) xrank_barrier(A, A.epoch + 2);
+    if (blockIdx.x == 0) xrank_barrier(A, epoch + 2);
     grid.sync();
 
     // all-gather of the other slices
@@ -110,7 +120,10 @@ __global__ void __launch_bounds__(256) k_allreduce(ArArgs A) {
         for (uint64_t u = lo + gtid; u < hi; u += gstride) A.my_y[u] = __ldcg(A.y[q] + u);
     }
     grid.sync();
-    if (blockIdx.x == 0) xrank_barrier(A, A.epoch + 3);
+    if (blockIdx.x == 0) {
+        xrank_barrier(A, epoch + 3);
+        if (threadIdx.x == 0) *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot) = epoch + 3;
+    }
 }
 
 }  // namespace lhc
@@ -122,7 +135,6 @@ struct lhc_comm {
     char* peers[lhc::kMaxRanks];
     void* opened[lhc::kMaxRanks];
     size_t bitmap_off, counters_off, signals_off, total;
-    uint32_t epoch;
     int grid;
 };
 
@@ -211,7 +223,6 @@ int lhc_comm_create(int rank, int world, const void* handles, const uint64_t* of
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_allreduce, 256, 0);
     c->grid = std::max(1, std::min(per_sm, 4)) * num_sms();
-    c->epoch = 0;
     *out = c;
     return LHC_OK;
 }
@@ -230,7 +241,6 @@ int sketch_allreduce(lhc_comm* c, void* stream) {
     A.my_y = reinterpret_cast<float4*>(c->local + c->counters_off);
     A.nb4 = align_up(c->p.m / 8, 16) / 16;
     A.nc4 = c->p.c / 4;
-    A.epoch = c->epoch;
     A.rank = c->rank;
     A.world = c->world;
     void* args[] = {(void*)&A};
@@ -238,7 +248,6 @@ int sketch_allreduce(lhc_comm* c, void* stream) {
                                                 args, 0, (cudaStream_t)stream);
     count_launch();
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "allreduce launch: %s", cudaGetErrorString(e));
-    c->epoch += 3;
     return LHC_OK;
 }
 

@@ -2,20 +2,24 @@
 // "the API makes ... Y <- sum Y and B <- OR B") as a hand-written NVLink P2P
 // all-reduce with mixed operators over CUDA-IPC-mapped peer buffers.
 //
-// Buffer of every rank: [bitmap (m/8 bytes, padded to 16) | counters (4c) | signals].
-// One cooperative kernel per call, two-shot:
-//   barrier A      every rank's compress has finished writing its buffer
-//   reduce-scatter rank r owns 1/G of each region; it loads that slice from all G
-//                  buffers over NVLink (128-bit loads), ORs the bitmap words /
-//                  sums the counters in ascending rank order, stores locally
-//   barrier B      every slice is reduced
-//   all-gather     rank r copies the G-1 other reduced slices from their owners
-//   barrier C      nobody reads our buffer any more (the caller may reuse it)
-// Barriers: block 0 publishes the epoch to every peer's signal slot with a
-// system-scope release store and spins on its own slots with acquire loads; the
-// rest of the grid waits at a grid-wide barrier.  The epoch counter is kept on
-// the device, so the call is CUDA-graph capturable and replayable.  Bytes per rank and direction:
-// 2(G-1)/G * S.
+// Buffer of every rank (lhc_comm_layout):
+//   [bitmap B | counters Y | staging for B | staging for Y | signals]
+// Each region is split into G contiguous slices of 16-byte units; rank q owns
+// slice q.  One cooperative kernel per call, two-shot, every NVLink transfer a
+// posted remote store (no remote loads):
+//   push 1   rank r writes its slice q of B and Y into rank q's staging, slot r,
+//            for every q != r                          ((G-1)/G * S bytes out)
+//   barrier 1
+//   reduce   rank q ORs / sums its own slice q with the G-1 staged copies in
+//            ascending rank order (the same fp32 order on every rank), stores it,
+//   push 2   and writes the reduced slice into every peer's B / Y   ((G-1)/G * S)
+//   barrier 2
+// No entry barrier is needed: push 1 only reads the caller's own sketch, and a
+// rank's staging is rewritten only after it has passed barrier 2 of the
+// previous call.  Barriers: every writing thread fences at system scope, the
+// grid syncs, then block 0 publishes the epoch to every peer's signal slot with a
+// system-scope release store and spins on its own slots with acquire loads.  The
+// epoch counter lives on the device, so a captured CUDA graph can be replayed.
 #include <cooperative_groups.h>
 #include <cuda.h>
 
@@ -29,14 +33,17 @@ namespace lhc {
 
 constexpr int kMaxRanks = 8;
 constexpr size_t kSignalBytes = 256;
+constexpr int kEpochSlot = 32;
+constexpr int kU = 4;  // 16-byte units per thread and pass
 
 struct ArArgs {
-    const uint4* b[kMaxRanks];  // bitmap region of every rank (own one included)
-    const float4* y[kMaxRanks]; // counter region of every rank
-    uint32_t* sig[kMaxRanks];   // signal slots of every rank
-    uint4* my_b;
-    float4* my_y;
-    uint64_t nb4, nc4;          // 16-byte units per region
+    uint4* b[kMaxRanks];    // B region of every rank (own one included)
+    float4* y[kMaxRanks];   // Y region of every rank
+    uint4* sb[kMaxRanks];   // B staging of every rank: G slots of sb_slot units
+    float4* sy[kMaxRanks];  // Y staging of every rank: G slots of sy_slot units
+    uint32_t* sig[kMaxRanks];
+    uint64_t nb4, nc4;      // 16-byte units per region
+    uint64_t sb_slot, sy_slot;
     int rank, world;
 };
 
@@ -49,19 +56,21 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
     return v;
 }
 
-// Cross-rank barrier, executed by block 0 only (the grid syncs around it).
-__device__ void xrank_barrier(const ArArgs& A, uint32_t epoch) {
-    const int t = threadIdx.x;
-    if (t < A.world && t != A.rank) {
-        __threadfence_system();
-        st_release_sys(A.sig[t] + A.rank, epoch);
-    }
-    if (t < A.world && t != A.rank) {
-        const uint32_t* mine = A.sig[A.rank] + t;
-        while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
+// Cross-rank barrier: all threads fence their remote stores, the grid syncs, block 0
+// exchanges flags, the grid syncs again.
+__device__ void xrank_barrier(cg::grid_group& grid, const ArArgs& A, uint32_t epoch) {
+    __threadfence_system();
+    grid.sync();
+    if (blockIdx.x == 0) {
+        const int t = threadIdx.x;
+        if (t < A.world && t != A.rank) st_release_sys(A.sig[t] + A.rank, epoch);
+        if (t < A.world && t != A.rank) {
+            const uint32_t* mine = A.sig[A.rank] + t;
+            while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
+            }
         }
     }
-    __syncthreads();
+    grid.sync();
 }
 
 __device__ __forceinline__ void slice(uint64_t n, int q, int world, uint64_t* lo, uint64_t* hi) {
@@ -69,61 +78,102 @@ __device__ __forceinline__ void slice(uint64_t n, int q, int world, uint64_t* lo
     *hi = n * (q + 1) / world;
 }
 
-// The barrier epoch lives in the rank's own signal area (slot kEpochSlot) and is
-// advanced by the kernel itself, so a captured CUDA graph can be replayed.
-constexpr int kEpochSlot = 32;
+__device__ __forceinline__ void combine(uint4& a, const uint4& v) {
+    a.x |= v.x; a.y |= v.y; a.z |= v.z; a.w |= v.w;
+}
+__device__ __forceinline__ void combine(float4& a, const float4& v) {
+    a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+}
 
+// push 1 for one region: my slice q -> rank q's staging slot `rank`
+template <int G, typename T>
+__device__ void push_slices(T* const* dst_stage, const T* src, uint64_t n, uint64_t slot, int rank,
+                            uint64_t gtid, uint64_t gstride) {
+#pragma unroll 1
+    for (int d = 1; d < G; d++) {
+        const int q = (rank + d) % G;  // stagger the destinations across ranks
+        uint64_t lo, hi;
+        slice(n, q, G, &lo, &hi);
+        T* out = dst_stage[q] + (uint64_t)rank * slot - lo;
+        for (uint64_t u0 = lo + gtid; u0 < hi; u0 += kU * gstride) {
+            T v[kU];
+#pragma unroll
+            for (int a = 0; a < kU; a++) {
+                const uint64_t u = u0 + a * gstride;
+                if (u < hi) v[a] = __ldcs(src + u);
+            }
+#pragma unroll
+            for (int a = 0; a < kU; a++) {
+                const uint64_t u = u0 + a * gstride;
+                if (u < hi) out[u] = v[a];
+            }
+        }
+    }
+}
+
+// reduce my slice (own + G-1 staged copies, ascending rank), store it locally and
+// into every peer's region
+template <int G, typename T>
+__device__ void reduce_push(T* const* region, const T* stage, uint64_t n, uint64_t slot, int rank,
+                            uint64_t gtid, uint64_t gstride) {
+    constexpr int U = G <= 2 ? 4 : G <= 4 ? 2 : 1;  // keeps U * G loads in flight
+    uint64_t lo, hi;
+    slice(n, rank, G, &lo, &hi);
+    for (uint64_t u0 = lo + gtid; u0 < hi; u0 += U * gstride) {
+        T v[U][G];
+#pragma unroll
+        for (int a = 0; a < U; a++) {
+            const uint64_t u = u0 + a * gstride;
+            if (u < hi) {
+#pragma unroll
+                for (int r = 0; r < G; r++)
+                    v[a][r] = r == rank ? __ldcg(region[rank] + u) : __ldcg(stage + r * slot + (u - lo));
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < U; a++) {
+            const uint64_t u = u0 + a * gstride;
+            if (u < hi) {
+                T acc = v[a][0];
+#pragma unroll
+                for (int r = 1; r < G; r++) combine(acc, v[a][r]);
+#pragma unroll
+                for (int d = 0; d < G; d++) region[(rank + d) % G][u] = acc;
+            }
+        }
+    }
+}
+
+#ifndef LHC_AR_TIMING
+#define LHC_AR_TIMING 0
+#endif
+// debug: block 0 stamps the phase boundaries into signal slots 40.. (u64 each)
+__device__ __forceinline__ void ar_stamp(const ArArgs& A, int k) {
+    if (LHC_AR_TIMING && blockIdx.x == 0 && threadIdx.x == 0)
+        reinterpret_cast<unsigned long long*>(A.sig[A.rank] + 40)[k] = globaltimer();
+}
+
+template <int G>
 __global__ void __launch_bounds__(256) k_allreduce(ArArgs A) {
     cg::grid_group grid = cg::this_grid();
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
-    __shared__ uint32_t sh_epoch;
-    if (blockIdx.x == 0) {
-        if (threadIdx.x == 0) sh_epoch = *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot);
-        __syncthreads();
-    }
-    const uint32_t epoch = blockIdx.x == 0 ? sh_epoch : 0u;
+    uint32_t epoch = 0;
+    if (blockIdx.x == 0) epoch = *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot);
 
-    if (blockIdx.x == 0) xrank_barrier(A, epoch + 1);
-    grid.sync();
-
-    // reduce-scatter of my slice
-    uint64_t lo, hi;
-    slice(A.nb4, A.rank, A.world, &lo, &hi);
-    for (uint64_t u = lo + gtid; u < hi; u += gstride) {
-        uint4 acc = __ldcg(A.b[0] + u);
-        for (int r = 1; r < A.world; r++) {
-            const uint4 v = __ldcg(A.b[r] + u);
-            acc.x |= v.x; acc.y |= v.y; acc.z |= v.z; acc.w |= v.w;
-        }
-        A.my_b[u] = acc;
-    }
-    slice(A.nc4, A.rank, A.world, &lo, &hi);
-    for (uint64_t u = lo + gtid; u < hi; u += gstride) {
-        float4 acc = __ldcg(A.y[0] + u);
-        for (int r = 1; r < A.world; r++) {
-            const float4 v = __ldcg(A.y[r] + u);
-            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-        A.my_y[u] = acc;
-    }
-    grid.sync();
-    if (blockIdx.x == 0) xrank_barrier(A, epoch + 2);
-    grid.sync();
-
-    // all-gather of the other slices
-    for (int q = 0; q < A.world; q++) {
-        if (q == A.rank) continue;
-        slice(A.nb4, q, A.world, &lo, &hi);
-        for (uint64_t u = lo + gtid; u < hi; u += gstride) A.my_b[u] = __ldcg(A.b[q] + u);
-        slice(A.nc4, q, A.world, &lo, &hi);
-        for (uint64_t u = lo + gtid; u < hi; u += gstride) A.my_y[u] = __ldcg(A.y[q] + u);
-    }
-    grid.sync();
-    if (blockIdx.x == 0) {
-        xrank_barrier(A, epoch + 3);
-        if (threadIdx.x == 0) *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot) = epoch + 3;
-    }
+    ar_stamp(A, 0);
+    push_slices<G>(A.sb, A.b[A.rank], A.nb4, A.sb_slot, A.rank, gtid, gstride);
+    push_slices<G>(A.sy, A.y[A.rank], A.nc4, A.sy_slot, A.rank, gtid, gstride);
+    ar_stamp(A, 1);
+    xrank_barrier(grid, A, epoch + 1);
+    ar_stamp(A, 2);
+    reduce_push<G>(A.b, A.sb[A.rank], A.nb4, A.sb_slot, A.rank, gtid, gstride);
+    reduce_push<G>(A.y, A.sy[A.rank], A.nc4, A.sy_slot, A.rank, gtid, gstride);
+    ar_stamp(A, 3);
+    xrank_barrier(grid, A, epoch + 2);
+    ar_stamp(A, 4);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot) = epoch + 2;
 }
 
 }  // namespace lhc
@@ -134,16 +184,23 @@ struct lhc_comm {
     char* local;
     char* peers[lhc::kMaxRanks];
     void* opened[lhc::kMaxRanks];
-    size_t bitmap_off, counters_off, signals_off, total;
+    size_t bitmap_off, counters_off, stage_b_off, stage_y_off, signals_off, total;
     int grid;
 };
 
 using namespace lhc;
 
-static void layout(const lhc_params* p, size_t* b, size_t* y, size_t* s, size_t* t) {
+// [B | Y | staging B | staging Y | signals]; a staging area holds G slots of
+// ceil(n/G) 16-byte units, at most n + kMaxRanks units for any G <= kMaxRanks.
+static uint64_t units_b(const lhc_params* p) { return align_up(p->m / 8, 16) / 16; }
+static uint64_t units_y(const lhc_params* p) { return p->c / 4; }
+static void layout(const lhc_params* p, size_t* b, size_t* y, size_t* sb, size_t* sy, size_t* s,
+                   size_t* t) {
     *b = 0;
     *y = align_up(p->m / 8, 256);
-    *s = align_up(*y + p->c * sizeof(float), 256);
+    *sb = align_up(*y + p->c * sizeof(float), 256);
+    *sy = align_up(*sb + (units_b(p) + kMaxRanks) * 16, 256);
+    *s = align_up(*sy + (units_y(p) + kMaxRanks) * 16, 256);
     *t = *s + kSignalBytes;
 }
 
@@ -152,8 +209,8 @@ extern "C" {
 int lhc_comm_layout(const lhc_params* p, size_t* bitmap_off, size_t* counters_off,
                     size_t* signals_off, size_t* total_bytes) {
     if (int rc = validate(p)) return rc;
-    size_t b, y, s, t;
-    layout(p, &b, &y, &s, &t);
+    size_t b, y, sb, sy, s, t;
+    layout(p, &b, &y, &sb, &sy, &s, &t);
     if (bitmap_off) *bitmap_off = b;
     if (counters_off) *counters_off = y;
     if (signals_off) *signals_off = s;
@@ -196,7 +253,8 @@ int lhc_comm_create(int rank, int world, const void* handles, const uint64_t* of
     c->world = world;
     c->p = *p;
     c->local = static_cast<char*>(local_buf);
-    layout(p, &c->bitmap_off, &c->counters_off, &c->signals_off, &c->total);
+    layout(p, &c->bitmap_off, &c->counters_off, &c->stage_b_off, &c->stage_y_off, &c->signals_off,
+           &c->total);
     if (buf_bytes < c->total) {
         const size_t need = c->total;
         delete c;
@@ -220,9 +278,18 @@ int lhc_comm_create(int rank, int world, const void* handles, const uint64_t* of
         c->opened[q] = ptr;
         c->peers[q] = static_cast<char*>(ptr) + offsets[q];
     }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_allreduce, 256, 0);
-    c->grid = std::max(1, std::min(per_sm, 4)) * num_sms();
+    // one grid size that is co-resident for every instantiation
+    const void* fns[] = {(const void*)k_allreduce<2>, (const void*)k_allreduce<3>,
+                         (const void*)k_allreduce<4>, (const void*)k_allreduce<5>,
+                         (const void*)k_allreduce<6>, (const void*)k_allreduce<7>,
+                         (const void*)k_allreduce<8>};
+    int per_sm = 4;
+    for (const void* f : fns) {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, 256, 0);
+        per_sm = std::min(per_sm, n);
+    }
+    c->grid = std::max(1, per_sm) * num_sms();
     *out = c;
     return LHC_OK;
 }
@@ -232,20 +299,33 @@ int sketch_allreduce(lhc_comm* c, void* stream) {
     reset_launches();
     if (c->world == 1) return LHC_OK;
     ArArgs A{};
+    const uint64_t nb4 = units_b(&c->p), nc4 = units_y(&c->p);
     for (int q = 0; q < c->world; q++) {
-        A.b[q] = reinterpret_cast<const uint4*>(c->peers[q] + c->bitmap_off);
-        A.y[q] = reinterpret_cast<const float4*>(c->peers[q] + c->counters_off);
+        A.b[q] = reinterpret_cast<uint4*>(c->peers[q] + c->bitmap_off);
+        A.y[q] = reinterpret_cast<float4*>(c->peers[q] + c->counters_off);
+        A.sb[q] = reinterpret_cast<uint4*>(c->peers[q] + c->stage_b_off);
+        A.sy[q] = reinterpret_cast<float4*>(c->peers[q] + c->stage_y_off);
         A.sig[q] = reinterpret_cast<uint32_t*>(c->peers[q] + c->signals_off);
     }
-    A.my_b = reinterpret_cast<uint4*>(c->local + c->bitmap_off);
-    A.my_y = reinterpret_cast<float4*>(c->local + c->counters_off);
-    A.nb4 = align_up(c->p.m / 8, 16) / 16;
-    A.nc4 = c->p.c / 4;
+    A.nb4 = nb4;
+    A.nc4 = nc4;
+    A.sb_slot = (nb4 + c->world - 1) / c->world;
+    A.sy_slot = (nc4 + c->world - 1) / c->world;
     A.rank = c->rank;
     A.world = c->world;
     void* args[] = {(void*)&A};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_allreduce, dim3(c->grid), dim3(256),
-                                                args, 0, (cudaStream_t)stream);
+    const void* fns[kMaxRanks + 1] = {nullptr,
+                                      nullptr,
+                                      (const void*)k_allreduce<2>,
+                                      (const void*)k_allreduce<3>,
+                                      (const void*)k_allreduce<4>,
+                                      (const void*)k_allreduce<5>,
+                                      (const void*)k_allreduce<6>,
+                                      (const void*)k_allreduce<7>,
+                                      (const void*)k_allreduce<8>};
+    const void* fn = fns[c->world];
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(c->grid), dim3(256), args, 0,
+                                                (cudaStream_t)stream);
     count_launch();
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "allreduce launch: %s", cudaGetErrorString(e));
     return LHC_OK;

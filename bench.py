@@ -307,9 +307,6 @@ def main():
         dec.peel(run.sketch)
         cnt()
         mark("peel")
-        dec.densify()
-        cnt()
-        mark("densify")
 
     def barrier():
         if world > 1:
@@ -325,8 +322,7 @@ def main():
     trace('timed')
     # ---- timed region: K steps, per-step events, L2 flushed between steps ----
     clocks = ClockSampler(local_rank)
-    phase = {"compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "query": 0.0, "peel": 0.0,
-             "densify": 0.0}
+    phase = {"compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "query": 0.0, "peel": 0.0}
     compress_launch_ms = []
     launches = [0]
     total_ms = 0.0
@@ -464,8 +460,8 @@ def main():
         "k_allreduce": (2 * (world - 1) / world * S, 1 if world > 1 else 0,
                         per_step_ms["allreduce"], nvl, "nvlink"),
         "k_query": (int(p.m) // 8 + 4 * n_c, 1, per_step_ms["query"], hbm, "hbm"),
-        "k_peel": (16 * int(p.c) + 9 * n_c, 1, per_step_ms["peel"], hbm, "hbm"),
-        "k_densify": (4 * wl.d + 4 * n_c, 1, per_step_ms["densify"], hbm, "hbm"),
+        # peel + finalize, and the dense output (zeroed, then the values at candidates)
+        "k_peel": (16 * int(p.c) + 9 * n_c + 4 * wl.d, 1, per_step_ms["peel"], hbm, "hbm"),
     }
     kernels = {}
     for name, (byts, nl, ms_l, peak, bound) in kern.items():

@@ -177,18 +177,17 @@ int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* 
                       float* out_val, uint8_t* out_peeled, float* out_dense, lhc_stats* stats,
                       void* stream);
 
-/* sketch_decompress in three stream-ordered steps sharing one workspace (call
- * them in this order with the same ws, cap_cand and outputs):
- *   sketch_query    step 1 — candidates to out_idx, n_cand/overflow to stats
- *   sketch_peel     steps 2-3 — out_val, out_peeled, n_peeled/rounds/success
- *   sketch_densify  out_dense (needs out_val); optional */
+/* sketch_decompress in two stream-ordered steps sharing one workspace (call
+ * them in this order with the same ws and cap_cand):
+ *   sketch_query  step 1 — candidates to out_idx, n_cand / overflow to stats
+ *   sketch_peel   steps 2-3 — out_val, out_peeled, n_peeled / rounds / success,
+ *                 and out_dense (nullable; the workspace holds a dense scratch
+ *                 used when it is NULL): zeroed, then the values at candidates */
 int sketch_query(const lhc_params* p, const uint32_t* bitmap, void* ws, size_t ws_bytes,
                  uint64_t cap_cand, uint32_t* out_idx, lhc_stats* stats, void* stream);
 int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_bytes,
                 uint64_t cap_cand, const uint32_t* out_idx, float* out_val, uint8_t* out_peeled,
-                lhc_stats* stats, void* stream);
-int sketch_densify(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t cap_cand,
-                   const float* out_val, float* out_dense, void* stream);
+                float* out_dense, lhc_stats* stats, void* stream);
 
 /* Number of kernel launches the last successful call of each entry point made
  * on this thread (bench accounting of `gpu_launches`). */

@@ -23,7 +23,6 @@ from ._lib import (  # noqa: F401
     sketch_compress,
     sketch_compress_coo,
     sketch_decompress,
-    sketch_densify,
     sketch_peel,
     sketch_query,
     sketch_hash_rows,

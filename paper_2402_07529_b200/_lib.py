@@ -78,7 +78,7 @@ EXPORTS = [
     "sketch_hash_rows", "sketch_clear", "sketch_compress", "sketch_compress_coo",
     "sketch_aggregate", "lhc_comm_layout", "lhc_ipc_handle", "lhc_comm_create",
     "sketch_allreduce", "lhc_comm_destroy", "sketch_decompress", "lhc_last_launch_count",
-    "sketch_query", "sketch_peel", "sketch_densify",
+    "sketch_query", "sketch_peel",
 ]
 
 
@@ -111,8 +111,7 @@ def lib() -> ctypes.CDLL:
             "sketch_decompress": (i32, [P, vp, vp, vp, sz, u64, vp, vp, vp, vp, vp, vp]),
             "lhc_last_launch_count": (i32, []),
             "sketch_query": (i32, [P, vp, vp, sz, u64, vp, vp, vp]),
-            "sketch_peel": (i32, [P, vp, vp, sz, u64, vp, vp, vp, vp, vp]),
-            "sketch_densify": (i32, [P, vp, sz, u64, vp, vp, vp]),
+            "sketch_peel": (i32, [P, vp, vp, sz, u64, vp, vp, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -239,22 +238,16 @@ def sketch_query(p: lhc_params, bitmap, ws, cap_cand, out_idx, stats, stream=Non
         _dev(stats, torch.uint8, STATS_BYTES, "stats"), _stream(stream)))
 
 
-def sketch_peel(p: lhc_params, counters, ws, cap_cand, out_idx, out_val, out_peeled, stats,
-                stream=None):
+def sketch_peel(p: lhc_params, counters, ws, cap_cand, out_idx, out_val, out_peeled, out_dense,
+                stats, stream=None):
     _check("sketch_peel", lib().sketch_peel(
         ctypes.byref(p), _dev(counters, torch.float32, p.c, "counters"),
         _dev(ws, torch.uint8, None, "ws"), ws.numel(), int(cap_cand),
         _dev(out_idx, torch.int32, cap_cand, "out_idx"),
         _dev(out_val, torch.float32, cap_cand, "out_val"),
         _dev(out_peeled, torch.uint8, cap_cand, "out_peeled"),
+        _dev(out_dense, torch.float32, p.d, "out_dense"),
         _dev(stats, torch.uint8, STATS_BYTES, "stats"), _stream(stream)))
-
-
-def sketch_densify(p: lhc_params, ws, cap_cand, out_val, out_dense, stream=None):
-    _check("sketch_densify", lib().sketch_densify(
-        ctypes.byref(p), _dev(ws, torch.uint8, None, "ws"), ws.numel(), int(cap_cand),
-        _dev(out_val, torch.float32, cap_cand, "out_val"),
-        _dev(out_dense, torch.float32, p.d, "out_dense"), _stream(stream)))
 
 
 def lhc_comm_layout(p: lhc_params):

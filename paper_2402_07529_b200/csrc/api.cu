@@ -94,13 +94,13 @@ WsLayout ws_layout(const KParams& P, uint64_t cap) {
     W.ctrl = o;      o = align_up(o + sizeof(Ctrl), 256);
     W.tabS = o;      o = align_up(o + nrows * P.k * sizeof(uint2), 256);
     W.gmask = o;     o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);
-    W.woff = o;      o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);
     W.chunk_cnt = o; o = align_up(o + (size_t)W.nchunks * sizeof(uint32_t), 256);
     W.chunk_off = o; o = align_up(o + (size_t)W.nchunks * sizeof(uint32_t), 256);
     W.cta_total = o; o = align_up(o + kMaxQueryCtas * sizeof(uint32_t), 256);
     W.cells = o;     o = align_up(o + P.c * sizeof(CellState), 256);
     W.claim = o;     o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);  // 1 bit per coordinate
     W.frontier = o;  o = align_up(o + P.c * sizeof(uint2), 256);
+    W.dense = o;     o = align_up(o + (size_t)W.nchunks * kTile * sizeof(float), 256);
     W.total = o;
     return W;
 }
@@ -190,9 +190,10 @@ struct WsView {
     WsLayout W;
     Ctrl* ctrl;
     uint2* tabS;
-    uint32_t *gmask, *woff, *chunk_cnt, *chunk_off, *cta_total, *claim;
+    uint32_t *gmask, *chunk_cnt, *chunk_off, *cta_total, *claim;
     CellState* cells;
     uint2* frontier;
+    float* dense;
 };
 
 int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, WsView* v) {
@@ -208,13 +209,13 @@ int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, 
     v->ctrl = reinterpret_cast<Ctrl*>(b + v->W.ctrl);
     v->tabS = reinterpret_cast<uint2*>(b + v->W.tabS);
     v->gmask = reinterpret_cast<uint32_t*>(b + v->W.gmask);
-    v->woff = reinterpret_cast<uint32_t*>(b + v->W.woff);
     v->chunk_cnt = reinterpret_cast<uint32_t*>(b + v->W.chunk_cnt);
     v->chunk_off = reinterpret_cast<uint32_t*>(b + v->W.chunk_off);
     v->cta_total = reinterpret_cast<uint32_t*>(b + v->W.cta_total);
     v->cells = reinterpret_cast<CellState*>(b + v->W.cells);
     v->claim = reinterpret_cast<uint32_t*>(b + v->W.claim);
     v->frontier = reinterpret_cast<uint2*>(b + v->W.frontier);
+    v->dense = reinterpret_cast<float*>(b + v->W.dense);
     return LHC_OK;
 }
 }  // namespace
@@ -231,37 +232,29 @@ int sketch_query(const lhc_params* p, const uint32_t* bitmap, void* ws, size_t w
     if (cudaMemsetAsync(v.ctrl, 0, sizeof(Ctrl), s) != cudaSuccess) return check_launch("memset");
     if (cudaMemsetAsync(stats, 0, sizeof(lhc_stats), s) != cudaSuccess) return check_launch("memset");
     cudaError_t e = launch_query(v.P, bitmap, v.tabS, v.gmask, v.chunk_cnt, v.chunk_off, v.cta_total,
-                                 v.woff, cap_cand, out_idx, v.ctrl, stats, s);
+                                 cap_cand, out_idx, v.ctrl, stats, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "query launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_query");
 }
 
 int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_bytes,
                 uint64_t cap_cand, const uint32_t* out_idx, float* out_val, uint8_t* out_peeled,
-                lhc_stats* stats, void* stream) {
+                float* out_dense, lhc_stats* stats, void* stream) {
     reset_launches();
     WsView v;
     if (int rc = ws_view(p, ws, ws_bytes, &cap_cand, &v)) return rc;
     if (!counters || !stats) return set_error(LHC_EINVAL, "NULL buffer");
     if (!aligned16(counters)) return set_error(LHC_EINVAL, "counters must be 16-byte aligned");
+    if (out_dense && !aligned16(out_dense)) return set_error(LHC_EINVAL, "out_dense must be 16-byte aligned");
     if (cap_cand && (!out_idx || !out_val || !out_peeled)) return set_error(LHC_EINVAL, "NULL output");
-    cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, v.gmask, v.woff, cap_cand, v.cells,
-                                v.claim, v.frontier, v.ctrl, out_val, out_peeled, stats,
-                                (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    float* dense = out_dense ? out_dense : v.dense;
+    if (cudaMemsetAsync(dense, 0, (size_t)p->d * sizeof(float), s) != cudaSuccess)
+        return check_launch("memset");
+    cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, dense, cap_cand, v.cells, v.claim,
+                                v.frontier, v.ctrl, out_val, out_peeled, stats, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_peel");
-}
-
-int sketch_densify(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t cap_cand,
-                   const float* out_val, float* out_dense, void* stream) {
-    reset_launches();
-    WsView v;
-    if (int rc = ws_view(p, ws, ws_bytes, &cap_cand, &v)) return rc;
-    if (!out_dense) return set_error(LHC_EINVAL, "NULL out_dense");
-    if (!aligned16(out_dense)) return set_error(LHC_EINVAL, "out_dense must be 16-byte aligned");
-    if (cap_cand && !out_val) return set_error(LHC_EINVAL, "NULL out_val");
-    launch_densify(v.P, v.gmask, v.woff, cap_cand, out_val, out_dense, (cudaStream_t)stream);
-    return check_launch("sketch_densify");
 }
 
 int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* counters,
@@ -271,13 +264,9 @@ int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* 
     if (int rc = sketch_query(p, bitmap, ws, ws_bytes, cap_cand, out_idx, stats, stream)) return rc;
     int n = lhc_last_launch_count();
     if (int rc = sketch_peel(p, counters, ws, ws_bytes, cap_cand, out_idx, out_val, out_peeled,
-                             stats, stream))
+                             out_dense, stats, stream))
         return rc;
     n += lhc_last_launch_count();
-    if (out_dense) {
-        if (int rc = sketch_densify(p, ws, ws_bytes, cap_cand, out_val, out_dense, stream)) return rc;
-        n += lhc_last_launch_count();
-    }
     reset_launches();
     count_launch(n);
     return LHC_OK;

@@ -24,21 +24,19 @@ void launch_clear(uint32_t* bitmap, uint64_t n_words, float* counters, uint64_t 
 void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* const* bitmaps,
                       const float* const* counters, uint32_t* out_bitmap, float* out_counters,
                       cudaStream_t s);
-// query + compaction + densify (query.cu)
+// query + compaction (query.cu)
 constexpr uint32_t kMaxQueryCtas = 4096;
 cudaError_t launch_query(const KParams& P, const uint32_t* bitmap, uint2* tabS, uint32_t* gmask,
                          uint32_t* chunk_cnt, uint32_t* chunk_off, uint32_t* cta_total,
-                         uint32_t* woff, uint64_t cap, uint32_t* out_idx, Ctrl* ctrl,
-                         lhc_stats* stats, cudaStream_t s);
+                         uint64_t cap, uint32_t* out_idx, Ctrl* ctrl, lhc_stats* stats,
+                         cudaStream_t s);
 uint32_t query_max_ctas();
-void launch_densify(const KParams& P, const uint32_t* gmask, const uint32_t* woff,
-                    uint64_t cap, const float* out_val, float* out_dense, cudaStream_t s);
+
 // peeling decoder (peel.cu)
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
-                        const uint32_t* cand, const uint32_t* gmask, const uint32_t* woff,
-                        uint64_t cap, CellState* cells, uint32_t* claim, uint2* frontier,
-                        Ctrl* ctrl, float* out_val, uint8_t* out_peeled, lhc_stats* stats,
-                        cudaStream_t s);
+                        const uint32_t* cand, float* dense, uint64_t cap, CellState* cells,
+                        uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* out_val,
+                        uint8_t* out_peeled, lhc_stats* stats, cudaStream_t s);
 
 WsLayout ws_layout(const KParams& P, uint64_t cap);
 

@@ -14,15 +14,18 @@
 //            be the only one left in several cells; a stale entry whose candidate
 //            was peeled meanwhile fails the claim), read val = sign * R[e] ("mapped by
 //            only one non-zero parameter"; "X_i can be deduced as
-//            g_j(i) * Y_h_j(i)"), write it to its slot (the query's per-word slot
-//            offset + rank in the word), and subtract sign_j * val and (2^32 + p)
-//            from the other cells of p ("deducting Y_h_j(i) by g_j(i) * X_i").  A cell
+//            g_j(i) * Y_h_j(i)"), write it to the dense output at p, and subtract
+//            sign_j * val and (2^32 + p) from the other cells of p ("deducting
+//            Y_h_j(i) by g_j(i) * X_i").  A cell
 //            whose degree drops from 2 to 1 is appended for the next round with
 //            its remaining candidate, which is the slot sum left in the key.  A
 //            round consumes only the segment the previous round appended, so the
 //            set of candidates peeled per round, and the number of rounds, are
 //            exactly those of synchronous peeling.
-//   finalize unpeeled candidates take the median over j of sign_j * R.
+//   finalize unpeeled candidates take the median over j of sign_j * R;
+//            the candidate list's values are gathered from the dense output.
+// The dense output is zeroed (stream-ordered memset) before the kernel, so every
+// non-candidate coordinate is exactly 0 without a separate densify pass.
 // Queue appends are aggregated per CTA in shared memory (one global atomic per
 // CTA per pass); every cell enters the queue at most once (c entries).
 #include <cooperative_groups.h>
@@ -89,10 +92,9 @@ __device__ __forceinline__ void flush_queue(uint2* sh_q, uint32_t* sh_n, uint32_
 template <int KT>
 __global__ void __launch_bounds__(kPeelThreads)
 k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
-       const uint32_t* __restrict__ cand, const uint32_t* __restrict__ gmask,
-       const uint32_t* __restrict__ woff, uint64_t cap, CellState* cells, uint32_t* claim,
-       uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val, uint8_t* __restrict__ out_peeled,
-       lhc_stats* stats) {
+       const uint32_t* __restrict__ cand, float* dense, uint64_t cap, CellState* cells,
+       uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
+       uint8_t* __restrict__ out_peeled, lhc_stats* stats) {
     cg::grid_group grid = cg::this_grid();
     constexpr uint32_t NJ = KT ? KT : kMaxK;
     // queue buffer: kPeelThreads * peel_q_per_thread(k) entries of dynamic smem
@@ -204,8 +206,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                 // issued back to back (volatile loads are not sunk into the branch): the
                 // claim (fetch-or of the candidate's bit: a candidate can be the only one
                 // left in several cells; a stale entry finds its bit already set), the
-                // pure cell's residual, the row maps and the slot of p (the query's
-                // per-word slot offset and mask)
+                // pure cell's residual and the row maps
                 const uint32_t bit = 1u << (p & 31);
                 const uint32_t old = atomicOr(claim + (p >> 5), bit);
                 const float Re = ld_cg_f32(&cells[e].R);
@@ -216,8 +217,6 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                     if (!KT && j >= k) break;
                     mp[j] = ld_nc_u2(row + j);
                 }
-                const uint32_t wo = ld_nc_u32(woff + (p >> 5));
-                const uint32_t wm = ld_nc_u32(gmask + (p >> 5));
                 if (!(old & bit)) {
                     const uint32_t t = p & (P.L - 1);
                     uint32_t ev[NJ];
@@ -229,7 +228,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                         if (ev[j] == e) ge = map_sign(mp[j]);
                     }
                     const float val = ge * Re;
-                    out_val[wo + __popc(wm & (bit - 1u))] = val;
+                    dense[p] = val;  // the value lands at its coordinate
                     atomicAdd(&sh_peeled, 1u);
                     // all reductions first (independent), then the queue appends
                     unsigned long long rest[NJ];
@@ -275,7 +274,10 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
         const uint32_t p = __ldg(cand + s);
         const bool pe = (__ldcg(claim + (p >> 5)) >> (p & 31)) & 1u;
         out_peeled[s] = pe ? 1 : 0;
-        if (!pe) {
+        float val;
+        if (pe) {
+            val = __ldcg(dense + p);
+        } else {
             float v[NJ];
             for (uint32_t j = 0; j < k; j++) {
                 uint32_t neg;
@@ -288,8 +290,10 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                 while (b >= 0 && v[b] > x) { v[b + 1] = v[b]; b--; }
                 v[b + 1] = x;
             }
-            out_val[s] = (k & 1) ? v[k / 2] : 0.5f * (v[k / 2 - 1] + v[k / 2]);
+            val = (k & 1) ? v[k / 2] : 0.5f * (v[k / 2 - 1] + v[k / 2]);
+            dense[p] = val;
         }
+        out_val[s] = val;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         stats->n_peeled = n_peeled;
@@ -314,17 +318,16 @@ static int peel_grid(int dev, uint32_t k) {
 }
 
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
-                        const uint32_t* cand, const uint32_t* gmask, const uint32_t* woff,
-                        uint64_t cap, CellState* cells, uint32_t* claim, uint2* frontier,
-                        Ctrl* ctrl, float* out_val, uint8_t* out_peeled, lhc_stats* stats,
-                        cudaStream_t s) {
+                        const uint32_t* cand, float* dense, uint64_t cap, CellState* cells,
+                        uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* out_val,
+                        uint8_t* out_peeled, lhc_stats* stats, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     KParams Pc = P;
     void* args[] = {(void*)&Pc,    (void*)&counters, (void*)&tabS,     (void*)&cand,
-                    (void*)&gmask, (void*)&woff,     (void*)&cap,      (void*)&cells,
-                    (void*)&claim, (void*)&frontier, (void*)&ctrl,     (void*)&out_val,
-                    (void*)&out_peeled, (void*)&stats};
+                    (void*)&dense, (void*)&cap,      (void*)&cells,    (void*)&claim,
+                    (void*)&frontier, (void*)&ctrl,  (void*)&out_val,  (void*)&out_peeled,
+                    (void*)&stats};
     cudaError_t err;
     if (P.k == 3)
         err = cudaLaunchCooperativeKernel((const void*)k_peel<3>, dim3(peel_grid<3>(dev, 3)),

@@ -1,7 +1,7 @@
 // query.cu — Phase II step 1 (a parameter is a candidate iff "all the
 // Bloom Filter's corresponding bits are set to one") on sm_100a: a streaming
 // Bloom query over all d coordinates with an ordered stream compaction of the
-// candidates, and the final densify (candidate values, exact zeros elsewhere).
+// candidates.
 //
 // Work unit: one lane = one 32-coordinate source word; one warp = one chunk of
 // 1024 coordinates; a CTA owns a contiguous range of 32-chunk tiles.  A source
@@ -15,7 +15,7 @@
 //   phase 1  candidate masks of every chunk -> gmask (d/8 bytes), per-chunk counts,
 //            per-CTA totals; also the Count Sketch row-map table for the peel
 //   phase 2  CTA prefix = sum of the totals of the CTAs before it; chunk offsets
-//            (kept for densify); candidates written in ascending order, one
+//            (kept in the workspace); candidates written in ascending order, one
 //            coalesced store per nonzero mask word.
 #include <cooperative_groups.h>
 
@@ -106,9 +106,8 @@ template <int KB>
 __global__ void __launch_bounds__(kQueryThreads)
 k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS,
         uint32_t* __restrict__ gmask, uint32_t* __restrict__ chunk_cnt,
-        uint32_t* __restrict__ chunk_off, uint32_t* __restrict__ cta_total,
-        uint32_t* __restrict__ woff, uint64_t cap, uint32_t* __restrict__ out_idx, Ctrl* ctrl,
-        lhc_stats* stats) {
+        uint32_t* __restrict__ chunk_off, uint32_t* __restrict__ cta_total, uint64_t cap,
+        uint32_t* __restrict__ out_idx, Ctrl* ctrl, lhc_stats* stats) {
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t sh_stage[kQueryWarps][kTile];
     __shared__ uint32_t sh_warp[kQueryWarps];
@@ -192,7 +191,6 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
             uint32_t tot;
             const uint32_t pre = warp_excl_scan(__popc(msk), lane, &tot);
             const unsigned long long out0 = tile_base + sh_chunk[cl];
-            woff[chunk * 32 + lane] = (uint32_t)(out0 + pre);  // slot of the word's first candidate
             const uint32_t chunk_q0 = (uint32_t)(chunk * kTile);
             const uint32_t nz = __ballot_sync(kFull, msk != 0);
             uint32_t maxpop = __popc(msk);
@@ -233,46 +231,6 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
     }
 }
 
-// Densify: out_dense[p] = out_val[slot(p)] at candidates, 0 elsewhere; streams
-// the candidate masks and per-word slot offsets, 128-bit streaming stores.
-__global__ void __launch_bounds__(256)
-k_densify(KParams P, const uint32_t* __restrict__ gmask, const uint32_t* __restrict__ woff,
-          uint64_t cap, const float* __restrict__ out_val, float* __restrict__ out_dense) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
-    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t chunk = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-         chunk < nchunks; chunk += warps) {
-        const uint32_t msk = __ldg(gmask + chunk * 32 + lane);
-        const uint32_t off = __ldg(woff + chunk * 32 + lane);
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const uint32_t g = lane + 32 * q;  // float4 group of the chunk
-            const uint32_t w = g >> 3, sh = (g & 7) * 4;
-            const uint32_t mw = __shfl_sync(kFull, msk, w);
-            const uint32_t ow = __shfl_sync(kFull, off, w);
-            const uint32_t nib = (mw >> sh) & 0xfu;
-            float o[4] = {0.f, 0.f, 0.f, 0.f};
-            if (nib) {
-                uint64_t slot = (uint64_t)ow + __popc(mw & ((1u << sh) - 1u));
-#pragma unroll
-                for (int e = 0; e < 4; e++)
-                    if (nib & (1u << e)) {
-                        o[e] = slot < cap ? out_val[slot] : 0.f;
-                        slot++;
-                    }
-            }
-            const uint64_t q0 = chunk * kTile + 4 * g;
-            if (q0 + 3 < P.d) {
-                __stcs(reinterpret_cast<float4*>(out_dense + q0), make_float4(o[0], o[1], o[2], o[3]));
-            } else {
-                for (int e = 0; e < 4; e++)
-                    if (q0 + e < P.d) out_dense[q0 + e] = o[e];
-            }
-        }
-    }
-}
-
 template <int KB>
 static int query_grid(int dev) {
     static int cached[64] = {0};
@@ -292,14 +250,14 @@ uint32_t query_max_ctas() {
 
 cudaError_t launch_query(const KParams& P, const uint32_t* bitmap, uint2* tabS, uint32_t* gmask,
                          uint32_t* chunk_cnt, uint32_t* chunk_off, uint32_t* cta_total,
-                         uint32_t* woff, uint64_t cap, uint32_t* out_idx, Ctrl* ctrl,
-                         lhc_stats* stats, cudaStream_t s) {
+                         uint64_t cap, uint32_t* out_idx, Ctrl* ctrl, lhc_stats* stats,
+                         cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     KParams Pc = P;
     void* args[] = {(void*)&Pc,        (void*)&bitmap,    (void*)&tabS,      (void*)&gmask,
-                    (void*)&chunk_cnt, (void*)&chunk_off, (void*)&cta_total, (void*)&woff,
-                    (void*)&cap,       (void*)&out_idx,   (void*)&ctrl,      (void*)&stats};
+                    (void*)&chunk_cnt, (void*)&chunk_off, (void*)&cta_total, (void*)&cap,
+                    (void*)&out_idx,   (void*)&ctrl,      (void*)&stats};
     cudaError_t e = P.kb == 3
         ? cudaLaunchCooperativeKernel((const void*)k_query<3>, dim3(query_grid<3>(dev)),
                                       dim3(kQueryThreads), args, 0, s)
@@ -307,14 +265,6 @@ cudaError_t launch_query(const KParams& P, const uint32_t* bitmap, uint2* tabS, 
                                       dim3(kQueryThreads), args, 0, s);
     count_launch();
     return e;
-}
-
-void launch_densify(const KParams& P, const uint32_t* gmask, const uint32_t* woff,
-                    uint64_t cap, const float* out_val, float* out_dense, cudaStream_t s) {
-    const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
-    uint32_t blocks = (uint32_t)std::min<uint64_t>((nchunks + 7) / 8, (uint64_t)num_sms() * 8);
-    k_densify<<<blocks, 256, 0, s>>>(P, gmask, woff, cap, out_val, out_dense);
-    count_launch();
 }
 
 }  // namespace lhc

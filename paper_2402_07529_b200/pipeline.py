@@ -63,17 +63,13 @@ class Decoder:
                             self.val, self.peeled, self.dense, self.stats, stream)
         return self
 
-    # the three steps of __call__, separately (for per-kernel timing)
+    # the two steps of __call__, separately (for per-kernel timing)
     def query(self, sketch: Sketch, stream=None):
         L.sketch_query(self.p, sketch.bitmap, self.ws, self.cap, self.idx, self.stats, stream)
 
     def peel(self, sketch: Sketch, stream=None):
         L.sketch_peel(self.p, sketch.counters, self.ws, self.cap, self.idx, self.val, self.peeled,
-                      self.stats, stream)
-
-    def densify(self, stream=None):
-        if self.dense is not None:
-            L.sketch_densify(self.p, self.ws, self.cap, self.val, self.dense, stream)
+                      self.dense, self.stats, stream)
 
     def read_stats(self) -> dict:
         return L.read_stats(self.stats)

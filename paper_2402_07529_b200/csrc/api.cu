@@ -94,8 +94,6 @@ WsLayout ws_layout(const KParams& P, uint64_t cap) {
     W.ctrl = o;      o = align_up(o + sizeof(Ctrl), 256);
     W.tabS = o;      o = align_up(o + nrows * P.k * sizeof(uint2), 256);
     W.gmask = o;     o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);
-    W.chunk_cnt = o; o = align_up(o + (size_t)W.nchunks * sizeof(uint32_t), 256);
-    W.chunk_off = o; o = align_up(o + (size_t)W.nchunks * sizeof(uint32_t), 256);
     W.cta_total = o; o = align_up(o + kMaxQueryCtas * sizeof(uint32_t), 256);
     W.cells = o;     o = align_up(o + P.c * sizeof(CellState), 256);
     W.claim = o;     o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);  // 1 bit per coordinate
@@ -190,7 +188,7 @@ struct WsView {
     WsLayout W;
     Ctrl* ctrl;
     uint2* tabS;
-    uint32_t *gmask, *chunk_cnt, *chunk_off, *cta_total, *claim;
+    uint32_t *gmask, *cta_total, *claim;
     CellState* cells;
     uint2* frontier;
     float* dense;
@@ -209,8 +207,6 @@ int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, 
     v->ctrl = reinterpret_cast<Ctrl*>(b + v->W.ctrl);
     v->tabS = reinterpret_cast<uint2*>(b + v->W.tabS);
     v->gmask = reinterpret_cast<uint32_t*>(b + v->W.gmask);
-    v->chunk_cnt = reinterpret_cast<uint32_t*>(b + v->W.chunk_cnt);
-    v->chunk_off = reinterpret_cast<uint32_t*>(b + v->W.chunk_off);
     v->cta_total = reinterpret_cast<uint32_t*>(b + v->W.cta_total);
     v->cells = reinterpret_cast<CellState*>(b + v->W.cells);
     v->claim = reinterpret_cast<uint32_t*>(b + v->W.claim);
@@ -231,8 +227,8 @@ int sketch_query(const lhc_params* p, const uint32_t* bitmap, void* ws, size_t w
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaMemsetAsync(v.ctrl, 0, sizeof(Ctrl), s) != cudaSuccess) return check_launch("memset");
     if (cudaMemsetAsync(stats, 0, sizeof(lhc_stats), s) != cudaSuccess) return check_launch("memset");
-    cudaError_t e = launch_query(v.P, bitmap, v.tabS, v.gmask, v.chunk_cnt, v.chunk_off, v.cta_total,
-                                 cap_cand, out_idx, v.ctrl, stats, s);
+    cudaError_t e = launch_query(v.P, bitmap, v.tabS, v.gmask, v.cta_total, cap_cand, out_idx,
+                                 v.ctrl, stats, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "query launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_query");
 }

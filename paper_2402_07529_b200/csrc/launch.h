@@ -27,9 +27,8 @@ void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* co
 // query + compaction (query.cu)
 constexpr uint32_t kMaxQueryCtas = 4096;
 cudaError_t launch_query(const KParams& P, const uint32_t* bitmap, uint2* tabS, uint32_t* gmask,
-                         uint32_t* chunk_cnt, uint32_t* chunk_off, uint32_t* cta_total,
-                         uint64_t cap, uint32_t* out_idx, Ctrl* ctrl, lhc_stats* stats,
-                         cudaStream_t s);
+                         uint32_t* cta_total, uint64_t cap, uint32_t* out_idx, Ctrl* ctrl,
+                         lhc_stats* stats, cudaStream_t s);
 uint32_t query_max_ctas();
 
 // peeling decoder (peel.cu)

@@ -4,7 +4,7 @@
 // candidates.
 //
 // Work unit: one lane = one 32-coordinate source word; one warp = one chunk of
-// 1024 coordinates; a CTA owns a contiguous range of 32-chunk tiles.  A source
+// 1024 coordinates; a CTA owns a contiguous range of chunks.  A source
 // word of input row i is the AND over probes j of destination row rowB_j(i) of B
 // rotated back by biasB_j(i): each lane loads word w of its row's destination row
 // (128 contiguous bytes per row for L = 1024; B is L2-resident) and the rotation
@@ -12,11 +12,11 @@
 // the lanes of the row (one hash per input row and probe).
 //
 // One cooperative kernel, one grid barrier:
-//   phase 1  candidate masks of every chunk -> gmask (d/8 bytes), per-chunk counts,
-//            per-CTA totals; also the Count Sketch row-map table for the peel
-//   phase 2  CTA prefix = sum of the totals of the CTAs before it; chunk offsets
-//            (kept in the workspace); candidates written in ascending order, one
-//            coalesced store per nonzero mask word.
+//   phase 1  candidate masks of every chunk -> gmask (d/8 bytes) and per-CTA
+//            totals; also the Count Sketch row-map table for the peel
+//   phase 2  CTA prefix = sum of the totals of the CTAs before it; then thread =
+//            word: a block scan of 256 word counts gives each word the slot of its
+//            first candidate and the thread writes them (ascending order).
 #include <cooperative_groups.h>
 
 #include "launch.h"
@@ -28,8 +28,8 @@ namespace lhc {
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kQueryThreads = 256;  // 8 warps
 constexpr int kQueryWarps = kQueryThreads / 32;
-constexpr int kChunksPerWarp = 4;   // 8 warps * 4 = 32 chunks per tile
-constexpr uint32_t kChunksPerTile = 32;
+constexpr int kChunksPerWarp = 4;
+constexpr uint32_t kStage = 12288;  // staged candidates per block of 1024 words (48 KB)
 
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t lane, uint32_t* total) {
     uint32_t x = v;
@@ -102,22 +102,67 @@ __device__ __forceinline__ void query_chunks(const KParams& P, const uint32_t* _
     }
 }
 
+// L = 1024 (one input row per chunk): masks of 8 chunks at once; the 8 * KB row
+// maps are hashed by 8 * KB lanes in parallel and each lane's 8 * KB destination
+// words are loaded back to back.
 template <int KB>
-__global__ void __launch_bounds__(kQueryThreads)
+__device__ __forceinline__ void query_chunks8_onerow(const KParams& P,
+                                                     const uint32_t* __restrict__ bitmap,
+                                                     uint64_t chunk0, uint64_t chunk_end,
+                                                     uint32_t lane, uint32_t out[8]) {
+    uint2 mine = make_uint2(0u, 0u);
+    if (lane < 8 * KB) {
+        const uint32_t cb = lane / KB, j = lane - cb * KB;
+        if (chunk0 + cb < chunk_end) mine = dom_map(P, 1, j, chunk0 + cb);
+    }
+    uint32_t dword[8][KB], bias[8][KB];
+#pragma unroll
+    for (int cb = 0; cb < 8; cb++) {
+#pragma unroll
+        for (int j = 0; j < KB; j++) {
+            const uint32_t rx = __shfl_sync(kFull, mine.x, cb * KB + j);
+            const uint32_t ry = __shfl_sync(kFull, mine.y, cb * KB + j);
+            bias[cb][j] = ry & 0x7fffffffu;
+            dword[cb][j] = chunk0 + cb < chunk_end ? __ldg(bitmap + (uint64_t)rx * 32 + lane) : 0u;
+        }
+    }
+#pragma unroll
+    for (int cb = 0; cb < 8; cb++) {
+        uint32_t res = chunk0 + cb < chunk_end ? kFull : 0u;
+#pragma unroll
+        for (int j = 0; j < KB; j++) {
+            const uint32_t db = (32 * lane + bias[cb][j]) & 1023u;
+            const uint32_t dw = db >> 5, dh = db & 31;
+            const uint32_t lo = __shfl_sync(kFull, dword[cb][j], dw);
+            const uint32_t hi = __shfl_sync(kFull, dword[cb][j], (dw + 1) & 31);
+            res &= dh ? (lo >> dh) | (hi << (32 - dh)) : lo;
+        }
+        const uint64_t q0 = ((chunk0 + cb) * 32 + lane) << 5;  // clear coordinates >= d
+        if (q0 >= P.d) res = 0u;
+        else if (q0 + 32 > P.d) res &= (1u << (uint32_t)(P.d - q0)) - 1u;
+        out[cb] = res;
+    }
+}
+
+// Phase 1 works on chunks (warp = chunk, lane = word), phase 2 on words (thread =
+// word): a block-wide scan of 256 word counts gives every word the slot of its
+// first candidate, and each thread writes its word's candidates.
+#ifndef LHC_QUERY_MINB
+#define LHC_QUERY_MINB 1
+#endif
+template <int KB>
+__global__ void __launch_bounds__(kQueryThreads, LHC_QUERY_MINB)
 k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS,
-        uint32_t* __restrict__ gmask, uint32_t* __restrict__ chunk_cnt,
-        uint32_t* __restrict__ chunk_off, uint32_t* __restrict__ cta_total, uint64_t cap,
+        uint32_t* __restrict__ gmask, uint32_t* __restrict__ cta_total, uint64_t cap,
         uint32_t* __restrict__ out_idx, Ctrl* ctrl, lhc_stats* stats) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint32_t sh_stage[kQueryWarps][kTile];
+    extern __shared__ uint32_t sh_stage[];  // kStage candidates
     __shared__ uint32_t sh_warp[kQueryWarps];
-    __shared__ uint32_t sh_chunk[kChunksPerTile];
     __shared__ unsigned long long sh_prefix;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
-    const uint64_t ntiles = (nchunks + kChunksPerTile - 1) / kChunksPerTile;
-    const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const uint64_t t_begin = blockIdx.x * per, t_end = min(ntiles, t_begin + per);
+    const uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;  // chunks per CTA
+    const uint64_t c_begin = min(nchunks, blockIdx.x * per), c_end = min(nchunks, c_begin + per);
 
     // Count Sketch row maps for the peel (grid-stride, independent of the query)
     {
@@ -129,25 +174,34 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
         }
     }
 
-    // phase 1: masks and counts
-    uint32_t my_total = 0;
-    for (uint64_t tile = t_begin; tile < t_end; tile++) {
-        const uint64_t c0 = tile * kChunksPerTile + warp * kChunksPerWarp;
-        uint32_t m[kChunksPerWarp];
-        query_chunks<KB>(P, bitmap, c0, lane, m);
+    // phase 1: masks of this CTA's chunks (warp w takes chunk groups w, w + 8, ...)
+    uint32_t my_cnt = 0;
+    if (KB != 0 && P.L == 1024) {
+        for (uint64_t c0 = c_begin + 8 * warp; c0 < c_end; c0 += 8 * kQueryWarps) {
+            uint32_t m[8];
+            query_chunks8_onerow<KB ? KB : 1>(P, bitmap, c0, c_end, lane, m);
 #pragma unroll
-        for (int it = 0; it < kChunksPerWarp; it++) {
-            const uint64_t chunk = c0 + it;
-            if (chunk < nchunks) {
-                gmask[chunk * 32 + lane] = m[it];
-                uint32_t cnt = __popc(m[it]);
-                for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
-                if (lane == 0) chunk_cnt[chunk] = cnt;
-                my_total += cnt;
-            }
+            for (int cb = 0; cb < 8; cb++)
+                if (c0 + cb < c_end) {
+                    gmask[(c0 + cb) * 32 + lane] = m[cb];
+                    my_cnt += __popc(m[cb]);
+                }
+        }
+    } else {
+        for (uint64_t c0 = c_begin + kChunksPerWarp * warp; c0 < c_end;
+             c0 += kChunksPerWarp * kQueryWarps) {
+            uint32_t m[kChunksPerWarp];
+            query_chunks<KB>(P, bitmap, c0, lane, m);
+#pragma unroll
+            for (int it = 0; it < kChunksPerWarp; it++)
+                if (c0 + it < c_end) {
+                    gmask[(c0 + it) * 32 + lane] = m[it];
+                    my_cnt += __popc(m[it]);
+                }
         }
     }
-    if (lane == 0) sh_warp[warp] = my_total;
+    for (int o = 16; o; o >>= 1) my_cnt += __shfl_xor_sync(kFull, my_cnt, o);
+    if (lane == 0) sh_warp[warp] = my_cnt;
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t t = 0;
@@ -168,59 +222,46 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
         __syncthreads();
     }
     unsigned long long run = sh_prefix;
-    for (uint64_t tile = t_begin; tile < t_end; tile++) {
-        // chunk offsets of the tile
-        if (warp == 0) {
-            const uint64_t chunk = tile * kChunksPerTile + lane;
-            const uint32_t cnt = chunk < nchunks ? __ldcg(chunk_cnt + chunk) : 0u;
-            uint32_t tot;
-            const uint32_t ex = warp_excl_scan(cnt, lane, &tot);
-            sh_chunk[lane] = ex;
-            if (chunk < nchunks) chunk_off[chunk] = (uint32_t)(run + ex);  // n_c < 2^32
-            if (lane == 0) sh_warp[0] = tot;
-        }
+    // blocks of 4 words per thread (16-byte loads); the candidates of a block are
+    // staged in shared memory (thread-serial over its bits) and copied out with
+    // coalesced stores, unless the block is denser than the staging buffer
+    const uint64_t w_begin = c_begin * 32, w_end = c_end * 32;  // multiples of 4
+    for (uint64_t w0 = w_begin; w0 < w_end; w0 += 4 * kQueryThreads) {
+        const uint64_t w = w0 + 4 * threadIdx.x;
+        uint4 m4 = make_uint4(0u, 0u, 0u, 0u);
+        if (w < w_end) m4 = __ldcg(reinterpret_cast<const uint4*>(gmask + w));
+        const uint32_t c0 = __popc(m4.x), c1 = __popc(m4.y), c2 = __popc(m4.z), c3 = __popc(m4.w);
+        uint32_t wt;
+        const uint32_t ex = warp_excl_scan(c0 + c1 + c2 + c3, lane, &wt);
+        __syncthreads();  // previous block's sh_warp / sh_stage readers are done
+        if (lane == 0) sh_warp[warp] = wt;
         __syncthreads();
-        const unsigned long long tile_base = run;
-        run += sh_warp[0];
-#pragma unroll 1
-        for (int it = 0; it < kChunksPerWarp; it++) {
-            const uint32_t cl = warp * kChunksPerWarp + it;
-            const uint64_t chunk = tile * kChunksPerTile + cl;
-            if (chunk >= nchunks) break;
-            const uint32_t msk = __ldcg(gmask + chunk * 32 + lane);
-            uint32_t tot;
-            const uint32_t pre = warp_excl_scan(__popc(msk), lane, &tot);
-            const unsigned long long out0 = tile_base + sh_chunk[cl];
-            const uint32_t chunk_q0 = (uint32_t)(chunk * kTile);
-            const uint32_t nz = __ballot_sync(kFull, msk != 0);
-            uint32_t maxpop = __popc(msk);
-            for (int o = 16; o; o >>= 1) maxpop = max(maxpop, __shfl_xor_sync(kFull, maxpop, o));
-            if ((uint32_t)__popc(nz) <= maxpop) {
-                // few, dense words: one coalesced store per nonzero word (its
-                // candidates are consecutive slots)
-                const uint32_t lt = (1u << lane) - 1u;
-                for (uint32_t z = nz; z; z &= z - 1) {
-                    const uint32_t w = __ffs(z) - 1;
-                    const uint32_t mw = __shfl_sync(kFull, msk, w);
-                    const uint32_t pw = __shfl_sync(kFull, pre, w);
-                    if (mw & (1u << lane)) {
-                        const unsigned long long pos = out0 + pw + __popc(mw & lt);
-                        if (pos < cap) out_idx[pos] = chunk_q0 + 32 * w + lane;
-                    }
-                }
-            } else {
-                // many sparse words: each lane stages its word's candidates in shared
-                // memory (max-popcount iterations), then a coalesced copy
-                uint32_t pos = pre;
-                for (uint32_t mm = msk; mm; mm &= mm - 1)
-                    sh_stage[warp][pos++] = chunk_q0 + 32 * lane + (__ffs(mm) - 1);
-                __syncwarp();
-                for (uint32_t a = lane; a < tot; a += 32)
-                    if (out0 + a < cap) out_idx[out0 + a] = sh_stage[warp][a];
-                __syncwarp();
-            }
+        uint32_t before = 0, all = 0;
+#pragma unroll
+        for (int v = 0; v < kQueryWarps; v++) {
+            const uint32_t x = sh_warp[v];
+            before += (uint32_t)v < warp ? x : 0u;
+            all += x;
         }
-        __syncthreads();
+        const uint32_t q0 = (uint32_t)(w << 5);
+        const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+        if (all <= kStage) {
+            uint32_t pos = before + ex;
+#pragma unroll
+            for (int k4 = 0; k4 < 4; k4++)
+                for (uint32_t mm = mw[k4]; mm; mm &= mm - 1)
+                    sh_stage[pos++] = q0 + 32 * k4 + (__ffs(mm) - 1);
+            __syncthreads();
+            for (uint32_t a = threadIdx.x; a < all; a += kQueryThreads)
+                if (run + a < cap) out_idx[run + a] = sh_stage[a];
+        } else {
+            unsigned long long pos = run + before + ex;
+#pragma unroll
+            for (int k4 = 0; k4 < 4; k4++)
+                for (uint32_t mm = mw[k4]; mm; mm &= mm - 1, pos++)
+                    if (pos < cap) out_idx[pos] = q0 + 32 * k4 + (__ffs(mm) - 1);
+        }
+        run += all;
     }
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
         const unsigned long long total = run;
@@ -235,8 +276,11 @@ template <int KB>
 static int query_grid(int dev) {
     static int cached[64] = {0};
     if (dev < 64 && cached[dev]) return cached[dev];
+    cudaFuncSetAttribute(k_query<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kStage * sizeof(uint32_t)));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<KB>, kQueryThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<KB>, kQueryThreads,
+                                                  kStage * sizeof(uint32_t));
     int g = std::max(1, per_sm) * num_sms();
     if (dev < 64) cached[dev] = g;
     return g;
@@ -249,20 +293,19 @@ uint32_t query_max_ctas() {
 }
 
 cudaError_t launch_query(const KParams& P, const uint32_t* bitmap, uint2* tabS, uint32_t* gmask,
-                         uint32_t* chunk_cnt, uint32_t* chunk_off, uint32_t* cta_total,
-                         uint64_t cap, uint32_t* out_idx, Ctrl* ctrl, lhc_stats* stats,
-                         cudaStream_t s) {
+                         uint32_t* cta_total, uint64_t cap, uint32_t* out_idx, Ctrl* ctrl,
+                         lhc_stats* stats, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     KParams Pc = P;
-    void* args[] = {(void*)&Pc,        (void*)&bitmap,    (void*)&tabS,      (void*)&gmask,
-                    (void*)&chunk_cnt, (void*)&chunk_off, (void*)&cta_total, (void*)&cap,
-                    (void*)&out_idx,   (void*)&ctrl,      (void*)&stats};
+    void* args[] = {(void*)&Pc,      (void*)&bitmap, (void*)&tabS, (void*)&gmask,
+                    (void*)&cta_total, (void*)&cap,  (void*)&out_idx, (void*)&ctrl,
+                    (void*)&stats};
     cudaError_t e = P.kb == 3
         ? cudaLaunchCooperativeKernel((const void*)k_query<3>, dim3(query_grid<3>(dev)),
-                                      dim3(kQueryThreads), args, 0, s)
+                                      dim3(kQueryThreads), args, kStage * sizeof(uint32_t), s)
         : cudaLaunchCooperativeKernel((const void*)k_query<0>, dim3(query_grid<0>(dev)),
-                                      dim3(kQueryThreads), args, 0, s);
+                                      dim3(kQueryThreads), args, kStage * sizeof(uint32_t), s);
     count_launch();
     return e;
 }

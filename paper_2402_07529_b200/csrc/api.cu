@@ -3,6 +3,7 @@
 // aggregate.cu, query.cu, peel.cu and comm.cu; nothing here touches data.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "launch.h"
@@ -23,6 +24,18 @@ int num_sms() {
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    if (dev < 64) cached[dev] = n;
+    return n;
+}
+
+int l2_bytes() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && cached[dev]) return cached[dev];
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrL2CacheSize, dev);
+    if (n <= 0) n = 126 << 20;
     if (dev < 64) cached[dev] = n;
     return n;
 }
@@ -99,6 +112,9 @@ WsLayout ws_layout(const KParams& P, uint64_t cap) {
     W.claim = o;     o = align_up(o + (size_t)W.nchunks * 32 * sizeof(uint32_t), 256);  // 1 bit per coordinate
     W.frontier = o;  o = align_up(o + P.c * sizeof(uint2), 256);
     W.dense = o;     o = align_up(o + (size_t)W.nchunks * kTile * sizeof(float), 256);
+    W.dst_off = o;   o = align_up(o + ((P.c >> P.log2L) + 1) * sizeof(uint32_t), 256);
+    W.pair_pos = o;  o = align_up(o + (size_t)P.nrows * P.k * sizeof(uint32_t), 256);
+    W.dst_list = o;  o = align_up(o + (size_t)P.nrows * P.k * sizeof(uint32_t), 256);
     W.total = o;
     return W;
 }
@@ -192,6 +208,7 @@ struct WsView {
     CellState* cells;
     uint2* frontier;
     float* dense;
+    uint32_t *dst_off, *pair_pos, *dst_list;
 };
 
 int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, WsView* v) {
@@ -212,6 +229,9 @@ int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, 
     v->claim = reinterpret_cast<uint32_t*>(b + v->W.claim);
     v->frontier = reinterpret_cast<uint2*>(b + v->W.frontier);
     v->dense = reinterpret_cast<float*>(b + v->W.dense);
+    v->dst_off = reinterpret_cast<uint32_t*>(b + v->W.dst_off);
+    v->pair_pos = reinterpret_cast<uint32_t*>(b + v->W.pair_pos);
+    v->dst_list = reinterpret_cast<uint32_t*>(b + v->W.dst_list);
     return LHC_OK;
 }
 }  // namespace
@@ -247,8 +267,22 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
     float* dense = out_dense ? out_dense : v.dense;
     if (cudaMemsetAsync(dense, 0, (size_t)p->d * sizeof(float), s) != cudaSuccess)
         return check_launch("memset");
+    if (cudaMemsetAsync(v.dst_off, 0, ((p->c >> v.P.log2L) + 1) * sizeof(uint32_t), s) != cudaSuccess ||
+        cudaMemsetAsync(v.claim, 0, ((size_t)p->d + 31) / 32 * sizeof(uint32_t), s) != cudaSuccess)
+        return check_launch("memset");
+    // cell state larger than half the L2: build it by destination row (no random
+    // HBM reductions); otherwise the in-kernel per-candidate insert is faster
+    // (LHC_CELL_BUILD=rows|insert overrides the choice; the results are identical)
+    int prebuilt = p->c * sizeof(CellState) > (size_t)l2_bytes() / 2 ? 1 : 0;
+    if (const char* ev = getenv("LHC_CELL_BUILD")) {
+        if (!strcmp(ev, "rows")) prebuilt = 1;
+        if (!strcmp(ev, "insert")) prebuilt = 0;
+    }
+    if (prebuilt)
+        launch_build_cells(v.P, counters, v.tabS, v.gmask, v.dst_off, v.pair_pos, v.dst_list,
+                           v.cells, s);
     cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, dense, cap_cand, v.cells, v.claim,
-                                v.frontier, v.ctrl, out_val, out_peeled, stats, s);
+                                v.frontier, v.ctrl, out_val, out_peeled, stats, prebuilt, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_peel");
 }

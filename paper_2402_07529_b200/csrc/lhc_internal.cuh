@@ -107,7 +107,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // Sub-allocation of the decompress workspace.
 struct WsLayout {
-    size_t tabS, gmask, cta_total, cells, claim, frontier, dense, ctrl, total;
+    size_t tabS, gmask, cta_total, cells, claim, frontier, dense, dst_off, pair_pos, dst_list, ctrl, total;
     uint32_t nchunks;
 };
 

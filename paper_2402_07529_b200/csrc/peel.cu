@@ -4,9 +4,11 @@
 //
 // One cooperative, persistent kernel (grid-wide barriers between phases) so that
 // the whole round loop runs on the device with no host round trips:
-//   init     cell state {key = 0, R = Y}; claim bits cleared
-//   insert   every candidate (coordinate p) adds (2^32 + p) to the key of each of
-//            its k cells: degree and coordinate sum in one 64-bit reduction
+//   build    cell state {key, R = Y} by destination row, without atomics on cells:
+//            the (input row, probe) pairs are counting-sorted by destination row;
+//            a warp per destination row rotates the query masks of its listed
+//            input rows and sums key = sum over its candidates p of (2^32 + p)
+//            (degree and coordinate sum) in shared memory, then writes the row once
 //   F0       every cell of degree one is appended to the frontier queue as the
 //            pair (cell, coordinate of its only candidate)
 //   rounds   (synchronous, reading R10) for every queue entry (e, p) of the
@@ -29,6 +31,8 @@
 // Queue appends are aggregated per CTA in shared memory (one global atomic per
 // CTA per pass); every cell enters the queue at most once (c entries).
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include "launch.h"
 
@@ -51,6 +55,40 @@ __device__ __forceinline__ uint32_t cand_cell(const KParams& P, const uint2* __r
     const uint2 mp = __ldg(tabS + i * P.k + j);
     *neg = mp.y >> 31;
     return (mp.x << P.log2L) + ((t + map_bias(mp)) & (P.L - 1));  // c < 2^32
+}
+
+constexpr int kRowsAhead = 8;  // listed rows whose mask words are loaded back to back
+
+// In-place exclusive scan of a[0..n) by one block (a[n-1] becomes the total when
+// the input's last element is 0).
+__device__ void block_excl_scan(uint32_t* a, uint32_t n, uint32_t* sh) {
+    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t b = threadIdx.x * per, e = min(n, b + per);
+    uint32_t sum = 0;
+    for (uint32_t t = b; t < e; t++) sum += a[t];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) sh[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (uint32_t w = 0; w < blockDim.x / 32; w++) {
+            const uint32_t v = sh[w];
+            sh[w] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    uint32_t run = sh[warp] + x - sum;
+    for (uint32_t t = b; t < e; t++) {
+        const uint32_t v = a[t];
+        a[t] = run;
+        run += v;
+    }
 }
 
 // queue-buffer entries per thread: a peel appends at most k - 1 cells, an F0
@@ -88,13 +126,137 @@ __device__ __forceinline__ void flush_queue(uint2* sh_q, uint32_t* sh_n, uint32_
     __syncthreads();
 }
 
+// ---- cell state by destination row, without atomics on cells ---------------------
+// (used when the cell state, 16 B per cell, does not fit in L2: then the
+// per-candidate 64-bit reductions of the in-kernel insert go to HBM at random)
+// The (input row i, probe j) pairs are counting-sorted by their destination row
+// D = row_j(i) of Y (count with reservations, one-block scan, scatter); then a warp
+// per destination row rotates the query masks of its listed input rows and sums
+// key = sum over the row's candidates p of (2^32 + p) (degree and coordinate sum)
+// in registers, lane w owning columns 32w .. 32w + 31, and writes the row's cells
+// {key, R = Y} once.
+__global__ void __launch_bounds__(256) k_pair_count(KParams P, const uint2* __restrict__ tabS,
+                                                    uint32_t* dst_off, uint32_t* pair_pos) {
+    const uint64_t n = (uint64_t)P.nrows * P.k;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
+         q += (uint64_t)gridDim.x * blockDim.x)
+        pair_pos[q] = atomicAdd(dst_off + __ldg(&tabS[q].x), 1u);
+}
+
+__global__ void __launch_bounds__(1024) k_pair_scan(uint32_t* dst_off, uint32_t n) {
+    __shared__ uint32_t sh[32];
+    block_excl_scan(dst_off, n, sh);
+}
+
+__global__ void __launch_bounds__(256) k_pair_scatter(KParams P, const uint2* __restrict__ tabS,
+                                                      const uint32_t* __restrict__ dst_off,
+                                                      const uint32_t* __restrict__ pair_pos,
+                                                      uint32_t* __restrict__ dst_list) {
+    const uint64_t n = (uint64_t)P.nrows * P.k;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n;
+         q += (uint64_t)gridDim.x * blockDim.x)
+        dst_list[dst_off[__ldg(&tabS[q].x)] + pair_pos[q]] = (uint32_t)(q / P.k);
+}
+
+__global__ void __launch_bounds__(256)
+k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
+              const uint32_t* __restrict__ gmask, const uint32_t* __restrict__ dst_off,
+              const uint32_t* __restrict__ dst_list, CellState* __restrict__ cells) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = P.nw;
+    const uint64_t nD = P.c >> P.log2L;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t D = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); D < nD;
+         D += warps) {
+        const uint32_t j = (uint32_t)(D / P.S_Y);
+        unsigned long long acc[32];
+#pragma unroll
+        for (int c = 0; c < 32; c++) acc[c] = 0ull;
+        const uint32_t l0 = dst_off[D], l1 = dst_off[D + 1];
+        for (uint32_t base = l0; base < l1; base += 32) {
+            // 32 listed rows at a time: lane r loads row r and its bias ...
+            const uint32_t n = min(32u, l1 - base);
+            const uint32_t my_i = lane < n ? dst_list[base + lane] : 0u;
+            const uint32_t my_b = lane < n ? map_bias(__ldg(tabS + (uint64_t)my_i * P.k + j)) : 0u;
+            // ... then kRowsAhead rows' mask words are loaded back to back
+            for (uint32_t r0 = 0; r0 < n; r0 += kRowsAhead) {
+                uint32_t mws[kRowsAhead], is[kRowsAhead], bs[kRowsAhead];
+#pragma unroll
+                for (int u = 0; u < kRowsAhead; u++) {
+                    is[u] = __shfl_sync(0xffffffffu, my_i, (r0 + u) & 31);
+                    bs[u] = __shfl_sync(0xffffffffu, my_b, (r0 + u) & 31);
+                    mws[u] = (r0 + u < n && lane < nw) ? __ldg(gmask + (uint64_t)is[u] * nw + lane) : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < kRowsAhead; u++) {
+                    // destination word w = lane takes source bits (32w - b) mod L ..
+                    const uint32_t b = bs[u];
+                    const uint32_t sb = (32 * lane + P.L - b) & (P.L - 1);
+                    const uint32_t sw = sb >> 5, sh = sb & 31;
+                    const uint32_t lo = __shfl_sync(0xffffffffu, mws[u], sw & (nw - 1));
+                    const uint32_t hi = __shfl_sync(0xffffffffu, mws[u], (sw + 1) & (nw - 1));
+                    const uint32_t dst = lane < nw ? (sh ? (lo >> sh) | (hi << (32 - sh)) : lo) : 0u;
+                    if (dst) {
+                        // coordinate of column 32w + c: i*L + (32w + c - b) mod L
+                        const uint64_t pbase = ((uint64_t)is[u] << P.log2L) + (1ull << 32);
+                        const uint32_t t0 = 32 * lane + P.L - b;
+#pragma unroll
+                        for (int c = 0; c < 32; c++)
+                            if (dst & (1u << c)) acc[c] += pbase + ((t0 + c) & (P.L - 1));
+                    }
+                }
+            }
+        }
+        if (lane < nw) {
+            const uint64_t e0 = (D << P.log2L) + 32 * lane;
+            const float4* y4 = reinterpret_cast<const float4*>(counters + e0);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const float4 y = __ldcs(y4 + q);
+                const float yv[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    CellState st;
+                    st.key = acc[4 * q + e];
+                    st.R = yv[e];
+                    st.pad = 0u;
+                    cells[e0 + 4 * q + e] = st;
+                }
+            }
+        }
+    }
+}
+
+void launch_build_cells(const KParams& P, const float* counters, const uint2* tabS,
+                        const uint32_t* gmask, uint32_t* dst_off, uint32_t* pair_pos,
+                        uint32_t* dst_list, CellState* cells, cudaStream_t s) {
+    const uint64_t npairs = (uint64_t)P.nrows * P.k;
+    const uint64_t nD = P.c >> P.log2L;
+    const uint32_t gp = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((npairs + 255) / 256, (uint64_t)num_sms() * 8));
+#ifdef LHC_DEBUG_SYNC
+#define DBG(name) { cudaError_t e_ = cudaStreamSynchronize(s); if (e_) fprintf(stderr, "%s: %s\n", name, cudaGetErrorString(e_)); else fprintf(stderr, "%s ok\n", name); }
+#else
+#define DBG(name)
+#endif
+    k_pair_count<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos);
+    DBG("pair_count");
+    k_pair_scan<<<1, 1024, 0, s>>>(dst_off, (uint32_t)nD + 1);
+    DBG("pair_scan");
+    k_pair_scatter<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos, dst_list);
+    DBG("pair_scatter");
+    const uint32_t gb = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((nD + 7) / 8, (uint64_t)num_sms() * 16));
+    k_build_cells<<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells);
+    DBG("build_cells");
+    count_launch(4);
+}
+
 // KT: compile-time k (3) or 0 for a run-time k <= kMaxK.
 template <int KT>
 __global__ void __launch_bounds__(kPeelThreads)
 k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
        const uint32_t* __restrict__ cand, float* dense, uint64_t cap, CellState* cells,
        uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
-       uint8_t* __restrict__ out_peeled, lhc_stats* stats) {
+       uint8_t* __restrict__ out_peeled, lhc_stats* stats, int prebuilt) {
     cg::grid_group grid = cg::this_grid();
     constexpr uint32_t NJ = KT ? KT : kMaxK;
     // queue buffer: kPeelThreads * peel_q_per_thread(k) entries of dynamic smem
@@ -116,10 +278,10 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
     if (threadIdx.x == 0) { sh_n = 0; sh_peeled = 0; }
     if (timer) ctrl->t[0] = globaltimer();
+    __syncthreads();
 
-    // init: cell state {0, Y} (coalesced: one 16-byte cell per lane, 4 passes
-    // unrolled so 4 loads are in flight), claim bits cleared
-    {
+    if (!prebuilt) {
+        // cell state {key = 0, R = Y} (coalesced, 4 loads in flight per thread) ...
         uint64_t e = gtid;
         for (; e + 3 * gstride < P.c; e += 4 * gstride) {
             float y[4];
@@ -141,25 +303,21 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
             st.pad = 0u;
             cells[e] = st;
         }
-    }
-    for (uint64_t w = gtid; w < ((uint64_t)P.d + 31) / 32; w += gstride) claim[w] = 0u;
-    grid.sync();
-    if (timer) ctrl->t[1] = globaltimer();
-
-    // insert: degree and coordinate sum of every cell
-    for (uint64_t s = gtid; s < n_c; s += gstride) {
-        const uint32_t p = __ldg(cand + s);
+        grid.sync();
+        // ... then every candidate p adds (2^32 + p) to the key of each of its cells
+        for (uint64_t s = gtid; s < n_c; s += gstride) {
+            const uint32_t p = __ldg(cand + s);
 #pragma unroll
-        for (uint32_t j = 0; j < NJ; j++) {
-            if (!KT && j >= k) break;
-            uint32_t neg;
-            const uint32_t e = cand_cell(P, tabS, p, j, &neg);
-            atomicAdd(&cells[e].key, (1ull << 32) + p);
+            for (uint32_t j = 0; j < NJ; j++) {
+                if (!KT && j >= k) break;
+                uint32_t neg;
+                const uint32_t e2 = cand_cell(P, tabS, p, j, &neg);
+                atomicAdd(&cells[e2].key, (1ull << 32) + p);
+            }
         }
-    }
-    grid.sync();
+        grid.sync();
+    }  // else: the cell state was built by destination row (k_build_cells)
     if (timer) ctrl->t[2] = globaltimer();
-
     // F0 ("round 0"): cells of degree one with their candidate, through rc[0]
     {
         // four cells per thread and pass (four loads in flight); one global
@@ -203,6 +361,13 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
             if (f < f_end) {
                 const uint2 ent = frontier[f];
                 const uint32_t e = ent.x, p = ent.y;
+#ifdef LHC_DEBUG_SYNC
+                if (e >= P.c || p >= P.d) {
+                    printf("bad frontier entry r=%u f=%llu e=%u p=%u (c=%llu d=%u)\n", r,
+                           (unsigned long long)f, e, p, (unsigned long long)P.c, P.d);
+                    continue;
+                }
+#endif
                 // issued back to back (volatile loads are not sunk into the branch): the
                 // claim (fetch-or of the candidate's bit: a candidate can be the only one
                 // left in several cells; a stale entry finds its bit already set), the
@@ -309,9 +474,10 @@ template <int KT>
 static int peel_grid(int dev, uint32_t k) {
     static int cached[64][kMaxK + 1] = {};
     if (dev < 64 && cached[dev][k]) return cached[dev][k];
-    cudaFuncSetAttribute(k_peel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)peel_smem(k));
+    const size_t smem = peel_smem(k);
+    cudaFuncSetAttribute(k_peel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel<KT>, kPeelThreads, peel_smem(k));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel<KT>, kPeelThreads, smem);
     int g = std::max(1, per_sm) * num_sms();
     if (dev < 64) cached[dev][k] = g;
     return g;
@@ -320,14 +486,17 @@ static int peel_grid(int dev, uint32_t k) {
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* cand, float* dense, uint64_t cap, CellState* cells,
                         uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* out_val,
-                        uint8_t* out_peeled, lhc_stats* stats, cudaStream_t s) {
+                        uint8_t* out_peeled, lhc_stats* stats, int prebuilt, cudaStream_t s) {
+#ifdef LHC_DEBUG_SYNC
+    if (getenv("LHC_DEBUG_SKIP_PEEL")) return cudaSuccess;
+#endif
     int dev = 0;
     cudaGetDevice(&dev);
     KParams Pc = P;
-    void* args[] = {(void*)&Pc,    (void*)&counters, (void*)&tabS,     (void*)&cand,
-                    (void*)&dense, (void*)&cap,      (void*)&cells,    (void*)&claim,
-                    (void*)&frontier, (void*)&ctrl,  (void*)&out_val,  (void*)&out_peeled,
-                    (void*)&stats};
+    void* args[] = {(void*)&Pc,    (void*)&counters, (void*)&tabS,    (void*)&cand,
+                    (void*)&dense, (void*)&cap,      (void*)&cells,   (void*)&claim,
+                    (void*)&frontier, (void*)&ctrl,  (void*)&out_val, (void*)&out_peeled,
+                    (void*)&stats, (void*)&prebuilt};
     cudaError_t err;
     if (P.k == 3)
         err = cudaLaunchCooperativeKernel((const void*)k_peel<3>, dim3(peel_grid<3>(dev, 3)),

@@ -206,6 +206,23 @@ def test_pipeline(lhc, ora, d, nnz, W, L, structure, law):
         assert np.array_equal(F(dec.dense), np.sum(np.stack(xs).astype(np.float64), axis=0))
 
 
+@pytest.mark.parametrize("build", ["rows", "insert"])
+@pytest.mark.parametrize("d,nnz,W,L,structure", CASES)
+def test_cell_build_paths(lhc, ora, d, nnz, W, L, structure, build, monkeypatch):
+    """Both ways of building the peeling state (per-candidate reductions, or by
+    destination row from the query masks) decode identically."""
+    monkeypatch.setenv("LHC_CELL_BUILD", build)
+    s = lhc.size_workload(d, nnz / d, W, L=L)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=0xB0B + d)
+    op = ora_params(ora, p)
+    xs = make_workers(d, nnz, W, 17 + d % 11, "dyadic", structure)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(op, xs)
+    compare_decode(ora, dec, ref, exact=True)
+
+
 @pytest.mark.parametrize("gamma", [0.9, 1.1, 1.2, 1.25, 1.5])
 def test_decode_threshold_sweep(lhc, ora, gamma):
     # near and below the peeling threshold: flags, rounds and the median fallback

@@ -271,18 +271,21 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
         cudaMemsetAsync(v.claim, 0, ((size_t)p->d + 31) / 32 * sizeof(uint32_t), s) != cudaSuccess)
         return check_launch("memset");
     // cell state larger than half the L2: build it by destination row (no random
-    // HBM reductions); otherwise the in-kernel per-candidate insert is faster
-    // (LHC_CELL_BUILD=rows|insert overrides the choice; the results are identical)
-    int prebuilt = p->c * sizeof(CellState) > (size_t)l2_bytes() / 2 ? 1 : 0;
+    // HBM reductions), compact (8 B/cell) when the input rows fit in 22 bits;
+    // otherwise the in-kernel per-candidate insert is faster.
+    // (LHC_CELL_BUILD=rows|compact|insert overrides the choice; results are identical)
+    int mode = p->c * sizeof(CellState) > (size_t)l2_bytes() / 2 ? 1 : 0;
+    if (mode == 1 && v.P.nrows <= (1u << 22)) mode = 2;
     if (const char* ev = getenv("LHC_CELL_BUILD")) {
-        if (!strcmp(ev, "rows")) prebuilt = 1;
-        if (!strcmp(ev, "insert")) prebuilt = 0;
+        if (!strcmp(ev, "rows")) mode = 1;
+        if (!strcmp(ev, "compact")) mode = v.P.nrows <= (1u << 22) ? 2 : 1;
+        if (!strcmp(ev, "insert")) mode = 0;
     }
-    if (prebuilt)
+    if (mode)
         launch_build_cells(v.P, counters, v.tabS, v.gmask, v.dst_off, v.pair_pos, v.dst_list,
-                           v.cells, s);
+                           v.cells, v.ctrl, mode == 2, s);
     cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, dense, cap_cand, v.cells, v.claim,
-                                v.frontier, v.ctrl, out_val, out_peeled, stats, prebuilt, s);
+                                v.frontier, v.ctrl, out_val, out_peeled, stats, mode, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_peel");
 }

@@ -34,11 +34,12 @@ uint32_t query_max_ctas();
 // peeling decoder (peel.cu)
 void launch_build_cells(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* gmask, uint32_t* dst_off, uint32_t* pair_pos,
-                        uint32_t* dst_list, CellState* cells, cudaStream_t s);
+                        uint32_t* dst_list, void* cells, Ctrl* ctrl, bool compact,
+                        cudaStream_t s);
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
-                        const uint32_t* cand, float* dense, uint64_t cap, CellState* cells,
+                        const uint32_t* cand, float* dense, uint64_t cap, void* cells,
                         uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* out_val,
-                        uint8_t* out_peeled, lhc_stats* stats, int prebuilt, cudaStream_t s);
+                        uint8_t* out_peeled, lhc_stats* stats, int mode, cudaStream_t s);
 int l2_bytes();
 
 WsLayout ws_layout(const KParams& P, uint64_t cap);

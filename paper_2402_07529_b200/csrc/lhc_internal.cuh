@@ -79,6 +79,18 @@ struct __align__(16) CellState {
     uint32_t pad;
 };
 
+// Compact decode state (8 bytes): key = sum over the cell's unpeeled candidates of
+// (2^24 + input row i); degree 0 or 1 is exact (then the low 24 bits are the row
+// of the only candidate, its column follows from the cell's column and the row's
+// bias), degree >= 2 reads as >= 2 while degree * (2^24 + rows) < 2^32.  Used when
+// the state does not fit in L2, input rows < 2^22 and no destination row receives
+// more than kCompactMaxDeg input rows (checked on the device).
+struct __align__(8) CellC {
+    uint32_t key;
+    float R;
+};
+constexpr uint32_t kCompactMaxDeg = 200;
+
 // Control block of one decompress call (workspace, zeroed per call).
 struct Ctrl {
     unsigned long long n_cand;  // written by the query scan
@@ -90,6 +102,7 @@ struct Ctrl {
     // final, and block 0 resets it during round r + 2, when nobody uses it.
     unsigned long long rc[3];
     uint32_t rounds_dbg;
+    uint32_t compact_fail;  // set by k_build_cells<compact> when a row is too full
     // instrumentation (device globaltimer ns): t[0..3] phase starts, t[3 + r] start of
     // round r, t[kCtrlTimes-1] end of rounds; fsize[r] = queue segment of round r
     unsigned long long t[128];

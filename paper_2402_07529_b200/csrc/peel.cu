@@ -33,6 +33,7 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "launch.h"
 
@@ -158,10 +159,12 @@ __global__ void __launch_bounds__(256) k_pair_scatter(KParams P, const uint2* __
         dst_list[dst_off[__ldg(&tabS[q].x)] + pair_pos[q]] = (uint32_t)(q / P.k);
 }
 
+template <bool COMPACT>
 __global__ void __launch_bounds__(256)
 k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
               const uint32_t* __restrict__ gmask, const uint32_t* __restrict__ dst_off,
-              const uint32_t* __restrict__ dst_list, CellState* __restrict__ cells) {
+              const uint32_t* __restrict__ dst_list, void* __restrict__ cells_v, Ctrl* ctrl) {
+    using Acc = typename std::conditional<COMPACT, uint32_t, unsigned long long>::type;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nw = P.nw;
     const uint64_t nD = P.c >> P.log2L;
@@ -169,10 +172,11 @@ k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __rest
     for (uint64_t D = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); D < nD;
          D += warps) {
         const uint32_t j = (uint32_t)(D / P.S_Y);
-        unsigned long long acc[32];
+        Acc acc[32];
 #pragma unroll
-        for (int c = 0; c < 32; c++) acc[c] = 0ull;
+        for (int c = 0; c < 32; c++) acc[c] = 0;
         const uint32_t l0 = dst_off[D], l1 = dst_off[D + 1];
+        if (COMPACT && l1 - l0 > kCompactMaxDeg && lane == 0) atomicOr(&ctrl->compact_fail, 1u);
         for (uint32_t base = l0; base < l1; base += 32) {
             // 32 listed rows at a time: lane r loads row r and its bias ...
             const uint32_t n = min(32u, l1 - base);
@@ -197,12 +201,19 @@ k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __rest
                     const uint32_t hi = __shfl_sync(0xffffffffu, mws[u], (sw + 1) & (nw - 1));
                     const uint32_t dst = lane < nw ? (sh ? (lo >> sh) | (hi << (32 - sh)) : lo) : 0u;
                     if (dst) {
-                        // coordinate of column 32w + c: i*L + (32w + c - b) mod L
-                        const uint64_t pbase = ((uint64_t)is[u] << P.log2L) + (1ull << 32);
-                        const uint32_t t0 = 32 * lane + P.L - b;
+                        if (COMPACT) {
+                            const uint32_t add = (1u << 24) + is[u];
 #pragma unroll
-                        for (int c = 0; c < 32; c++)
-                            if (dst & (1u << c)) acc[c] += pbase + ((t0 + c) & (P.L - 1));
+                            for (int c = 0; c < 32; c++)
+                                if (dst & (1u << c)) acc[c] += add;
+                        } else {
+                            // coordinate of column 32w + c: i*L + (32w + c - b) mod L
+                            const uint64_t pbase = ((uint64_t)is[u] << P.log2L) + (1ull << 32);
+                            const uint32_t t0 = 32 * lane + P.L - b;
+#pragma unroll
+                            for (int c = 0; c < 32; c++)
+                                if (dst & (1u << c)) acc[c] += pbase + ((t0 + c) & (P.L - 1));
+                        }
                     }
                 }
             }
@@ -216,11 +227,18 @@ k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __rest
                 const float yv[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
-                    CellState st;
-                    st.key = acc[4 * q + e];
-                    st.R = yv[e];
-                    st.pad = 0u;
-                    cells[e0 + 4 * q + e] = st;
+                    if (COMPACT) {
+                        CellC st;
+                        st.key = (uint32_t)acc[4 * q + e];
+                        st.R = yv[e];
+                        static_cast<CellC*>(cells_v)[e0 + 4 * q + e] = st;
+                    } else {
+                        CellState st;
+                        st.key = acc[4 * q + e];
+                        st.R = yv[e];
+                        st.pad = 0u;
+                        static_cast<CellState*>(cells_v)[e0 + 4 * q + e] = st;
+                    }
                 }
             }
         }
@@ -229,7 +247,8 @@ k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __rest
 
 void launch_build_cells(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* gmask, uint32_t* dst_off, uint32_t* pair_pos,
-                        uint32_t* dst_list, CellState* cells, cudaStream_t s) {
+                        uint32_t* dst_list, void* cells, Ctrl* ctrl, bool compact,
+                        cudaStream_t s) {
     const uint64_t npairs = (uint64_t)P.nrows * P.k;
     const uint64_t nD = P.c >> P.log2L;
     const uint32_t gp = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((npairs + 255) / 256, (uint64_t)num_sms() * 8));
@@ -245,99 +264,69 @@ void launch_build_cells(const KParams& P, const float* counters, const uint2* ta
     k_pair_scatter<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos, dst_list);
     DBG("pair_scatter");
     const uint32_t gb = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((nD + 7) / 8, (uint64_t)num_sms() * 16));
-    k_build_cells<<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells);
+    if (compact)
+        k_build_cells<true><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl);
+    else
+        k_build_cells<false><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl);
     DBG("build_cells");
     count_launch(4);
 }
 
 // KT: compile-time k (3) or 0 for a run-time k <= kMaxK.
-template <int KT>
-__global__ void __launch_bounds__(kPeelThreads)
-k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
-       const uint32_t* __restrict__ cand, float* dense, uint64_t cap, CellState* cells,
-       uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
-       uint8_t* __restrict__ out_peeled, lhc_stats* stats, int prebuilt) {
+// The two decode-state layouts: 16-byte cells keyed by coordinate (2^32 + p) and
+// 8-byte cells keyed by input row (2^24 + i).  A frontier entry is (cell, id) with
+// id = p (wide) or i | j << 24 (compact, j = the cell's probe).
+template <bool COMPACT>
+struct Cells {
+    using T = typename std::conditional<COMPACT, CellC, CellState>::type;
+    using K = typename std::conditional<COMPACT, uint32_t, unsigned long long>::type;
+    static constexpr int kShift = COMPACT ? 24 : 32;
+    __device__ static K one(uint32_t id) { return ((K)1 << kShift) + (K)id; }
+    __device__ static uint32_t deg(K key) { return (uint32_t)(key >> kShift); }
+    __device__ static uint32_t low(K key) { return (uint32_t)(key & (((K)1 << kShift) - 1)); }
+};
+
+// F0, the synchronous rounds and the finalize, on either layout.
+template <int KT, bool COMPACT>
+__device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
+                          const uint32_t* __restrict__ cand, float* dense, void* cells_v,
+                          uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
+                          uint8_t* __restrict__ out_peeled, lhc_stats* stats, uint64_t n_c,
+                          uint2* sh_q, uint32_t* sh_n, uint32_t* sh_base, uint32_t* sh_peeled) {
+    using C = Cells<COMPACT>;
+    using Cell = typename C::T;
+    using K = typename C::K;
+    Cell* cells = static_cast<Cell*>(cells_v);
     cg::grid_group grid = cg::this_grid();
     constexpr uint32_t NJ = KT ? KT : kMaxK;
-    // queue buffer: kPeelThreads * peel_q_per_thread(k) entries of dynamic smem
-    extern __shared__ uint2 sh_q[];
-    __shared__ uint32_t sh_n, sh_base, sh_peeled;
     const uint32_t k = KT ? (uint32_t)KT : P.k;
-
-    const uint64_t n_c = *(volatile unsigned long long*)&ctrl->n_cand;
-    if (n_c > cap) {  // overflow: nothing is peeled (stats.overflow set by the query)
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            stats->n_peeled = 0;
-            stats->rounds = 0;
-            stats->success = 0;
-        }
-        return;
-    }
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
-    if (threadIdx.x == 0) { sh_n = 0; sh_peeled = 0; }
-    if (timer) ctrl->t[0] = globaltimer();
-    __syncthreads();
 
-    if (!prebuilt) {
-        // cell state {key = 0, R = Y} (coalesced, 4 loads in flight per thread) ...
-        uint64_t e = gtid;
-        for (; e + 3 * gstride < P.c; e += 4 * gstride) {
-            float y[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) y[u] = __ldcs(counters + e + u * gstride);
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                CellState st;
-                st.key = 0ull;
-                st.R = y[u];
-                st.pad = 0u;
-                cells[e + u * gstride] = st;
-            }
-        }
-        for (; e < P.c; e += gstride) {
-            CellState st;
-            st.key = 0ull;
-            st.R = __ldcs(counters + e);
-            st.pad = 0u;
-            cells[e] = st;
-        }
-        grid.sync();
-        // ... then every candidate p adds (2^32 + p) to the key of each of its cells
-        for (uint64_t s = gtid; s < n_c; s += gstride) {
-            const uint32_t p = __ldg(cand + s);
-#pragma unroll
-            for (uint32_t j = 0; j < NJ; j++) {
-                if (!KT && j >= k) break;
-                uint32_t neg;
-                const uint32_t e2 = cand_cell(P, tabS, p, j, &neg);
-                atomicAdd(&cells[e2].key, (1ull << 32) + p);
-            }
-        }
-        grid.sync();
-    }  // else: the cell state was built by destination row (k_build_cells)
-    if (timer) ctrl->t[2] = globaltimer();
     // F0 ("round 0"): cells of degree one with their candidate, through rc[0]
     {
         // four cells per thread and pass (four loads in flight); one global
         // reservation per buffer-full, not per pass
         const uint32_t qcap = kPeelThreads * peel_q_per_thread(k);  // entries of sh_q
         for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < P.c; base += 4 * gstride) {
-            unsigned long long key[4];
+            K key[4];
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const uint64_t e = base + u * gstride + threadIdx.x;
-                key[u] = e < P.c ? __ldcg(&cells[e].key) : 0ull;
+                key[u] = e < P.c ? __ldcg(&cells[e].key) : (K)0;
             }
 #pragma unroll
             for (int u = 0; u < 4; u++)
-                if ((key[u] >> 32) == 1ull)
-                    sh_q[atomicAdd(&sh_n, 1u)] =
-                        make_uint2((uint32_t)(base + u * gstride + threadIdx.x), (uint32_t)key[u]);
+                if (C::deg(key[u]) == 1u) {
+                    const uint32_t e = (uint32_t)(base + u * gstride + threadIdx.x);
+                    const uint32_t id = COMPACT ? C::low(key[u]) | (((e >> P.log2L) / P.S_Y) << 24)
+                                                : C::low(key[u]);
+                    sh_q[atomicAdd(sh_n, 1u)] = make_uint2(e, id);
+                }
             __syncthreads();
-            if (sh_n + 4 * kPeelThreads > qcap || base + 4 * gstride >= P.c)
-                flush_queue(sh_q, &sh_n, &sh_base, frontier, 0u, &ctrl->rc[0]);
+            if (*sh_n + 4 * kPeelThreads > qcap || base + 4 * gstride >= P.c)
+                flush_queue(sh_q, sh_n, sh_base, frontier, 0u, &ctrl->rc[0]);
         }
     }
     grid.sync();
@@ -360,30 +349,36 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
             const uint64_t f = base + threadIdx.x;
             if (f < f_end) {
                 const uint2 ent = frontier[f];
-                const uint32_t e = ent.x, p = ent.y;
-#ifdef LHC_DEBUG_SYNC
-                if (e >= P.c || p >= P.d) {
-                    printf("bad frontier entry r=%u f=%llu e=%u p=%u (c=%llu d=%u)\n", r,
-                           (unsigned long long)f, e, p, (unsigned long long)P.c, P.d);
-                    continue;
-                }
-#endif
+                const uint32_t e = ent.x;
                 // issued back to back (volatile loads are not sunk into the branch): the
+                // pure cell's residual, the row maps of the candidate's input row and the
                 // claim (fetch-or of the candidate's bit: a candidate can be the only one
-                // left in several cells; a stale entry finds its bit already set), the
-                // pure cell's residual and the row maps
-                const uint32_t bit = 1u << (p & 31);
-                const uint32_t old = atomicOr(claim + (p >> 5), bit);
+                // left in several cells; a stale entry finds its bit already set)
                 const float Re = ld_cg_f32(&cells[e].R);
-                const uint2* row = tabS + (uint64_t)(p >> P.log2L) * k;
+                const uint32_t i = COMPACT ? (ent.y & 0xffffffu) : (ent.y >> P.log2L);
+                const uint2* row = tabS + (uint64_t)i * k;
                 uint2 mp[NJ];
 #pragma unroll
                 for (uint32_t j = 0; j < NJ; j++) {
                     if (!KT && j >= k) break;
                     mp[j] = ld_nc_u2(row + j);
                 }
+                uint32_t p, t;
+                if (COMPACT) {  // column of the pure cell, rotated back by the row's bias
+                    const uint32_t jp = ent.y >> 24;
+                    uint32_t bj = 0;
+#pragma unroll
+                    for (uint32_t j = 0; j < NJ; j++)
+                        if (j == jp) bj = map_bias(mp[j]);
+                    t = ((e & (P.L - 1)) + P.L - bj) & (P.L - 1);
+                    p = (i << P.log2L) + t;
+                } else {
+                    p = ent.y;
+                    t = p & (P.L - 1);
+                }
+                const uint32_t bit = 1u << (p & 31);
+                const uint32_t old = atomicOr(claim + (p >> 5), bit);
                 if (!(old & bit)) {
-                    const uint32_t t = p & (P.L - 1);
                     uint32_t ev[NJ];
                     float ge = 1.f;
 #pragma unroll
@@ -394,35 +389,36 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                     }
                     const float val = ge * Re;
                     dense[p] = val;  // the value lands at its coordinate
-                    atomicAdd(&sh_peeled, 1u);
+                    atomicAdd(sh_peeled, 1u);
                     // all reductions first (independent), then the queue appends
-                    unsigned long long rest[NJ];
+                    const K dec = (K)0 - C::one(COMPACT ? i : p);
+                    K rest[NJ];
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
                         // the pure cell held only p: nothing reads its state again
                         if (ev[j] == e) continue;
                         atomicAdd(&cells[ev[j]].R, -map_sign(mp[j]) * val);
-                        rest[j] = atomicAdd(&cells[ev[j]].key, 0ull - ((1ull << 32) + p)) -
-                                  ((1ull << 32) + p);
+                        rest[j] = atomicAdd(&cells[ev[j]].key, dec) + dec;
                     }
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
-                        if (ev[j] != e && (rest[j] >> 32) == 1ull)
-                            sh_q[atomicAdd(&sh_n, 1u)] = make_uint2(ev[j], (uint32_t)rest[j]);
+                        if (ev[j] != e && C::deg(rest[j]) == 1u)
+                            sh_q[atomicAdd(sh_n, 1u)] =
+                                make_uint2(ev[j], COMPACT ? C::low(rest[j]) | (j << 24) : C::low(rest[j]));
                     }
                 }
             }
             if (LHC_PEEL_TIMING && threadIdx.x == 0 && r < kCtrlTimes)
                 atomicMax(&ctrl->tproc[r], globaltimer());
-            flush_queue(sh_q, &sh_n, &sh_base, frontier, f_end, rc);
+            flush_queue(sh_q, sh_n, sh_base, frontier, f_end, rc);
             if (LHC_PEEL_TIMING && threadIdx.x == 0 && r < kCtrlTimes)
                 atomicMax(&ctrl->tflush[r], globaltimer());
         }
-        if (threadIdx.x == 0 && sh_peeled) {
-            atomicAdd(rc, (unsigned long long)sh_peeled << 32);
-            sh_peeled = 0;
+        if (threadIdx.x == 0 && *sh_peeled) {
+            atomicAdd(rc, (unsigned long long)*sh_peeled << 32);
+            *sh_peeled = 0;
         }
         grid.sync();
         const unsigned long long rcv = *(volatile unsigned long long*)rc;
@@ -468,6 +464,87 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     }
 }
 
+// KT: compile-time k (3) or 0 for a run-time k <= kMaxK.  mode: 0 = build the wide
+// state here (per-candidate reductions), 1 = wide state prebuilt by destination
+// row, 2 = compact state prebuilt by destination row (falls back to mode 0 if the
+// build flagged a row with too many input rows).
+template <int KT>
+__global__ void __launch_bounds__(kPeelThreads)
+k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
+       const uint32_t* __restrict__ cand, float* dense, uint64_t cap, void* cells_v,
+       uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
+       uint8_t* __restrict__ out_peeled, lhc_stats* stats, int mode) {
+    cg::grid_group grid = cg::this_grid();
+    constexpr uint32_t NJ = KT ? KT : kMaxK;
+    // queue buffer: kPeelThreads * peel_q_per_thread(k) entries of dynamic smem
+    extern __shared__ uint2 sh_q[];
+    __shared__ uint32_t sh_n, sh_base, sh_peeled;
+    const uint32_t k = KT ? (uint32_t)KT : P.k;
+
+    const uint64_t n_c = *(volatile unsigned long long*)&ctrl->n_cand;
+    if (n_c > cap) {  // overflow: nothing is peeled (stats.overflow set by the query)
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            stats->n_peeled = 0;
+            stats->rounds = 0;
+            stats->success = 0;
+        }
+        return;
+    }
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
+    if (threadIdx.x == 0) { sh_n = 0; sh_peeled = 0; }
+    if (timer) ctrl->t[0] = globaltimer();
+    if (mode == 2 && *(volatile uint32_t*)&ctrl->compact_fail) mode = 0;  // uniform
+    __syncthreads();
+
+    if (mode == 0) {
+        CellState* cells = static_cast<CellState*>(cells_v);
+        // cell state {key = 0, R = Y} (coalesced, 4 loads in flight per thread) ...
+        uint64_t e = gtid;
+        for (; e + 3 * gstride < P.c; e += 4 * gstride) {
+            float y[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) y[u] = __ldcs(counters + e + u * gstride);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                CellState st;
+                st.key = 0ull;
+                st.R = y[u];
+                st.pad = 0u;
+                cells[e + u * gstride] = st;
+            }
+        }
+        for (; e < P.c; e += gstride) {
+            CellState st;
+            st.key = 0ull;
+            st.R = __ldcs(counters + e);
+            st.pad = 0u;
+            cells[e] = st;
+        }
+        grid.sync();
+        // ... then every candidate p adds (2^32 + p) to the key of each of its cells
+        for (uint64_t s = gtid; s < n_c; s += gstride) {
+            const uint32_t p = __ldg(cand + s);
+#pragma unroll
+            for (uint32_t j = 0; j < NJ; j++) {
+                if (!KT && j >= k) break;
+                uint32_t neg;
+                const uint32_t e2 = cand_cell(P, tabS, p, j, &neg);
+                atomicAdd(&cells[e2].key, (1ull << 32) + p);
+            }
+        }
+        grid.sync();
+    }
+    if (timer) ctrl->t[2] = globaltimer();
+    if (mode == 2)
+        peel_body<KT, true>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
+                            out_peeled, stats, n_c, sh_q, &sh_n, &sh_base, &sh_peeled);
+    else
+        peel_body<KT, false>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
+                             out_peeled, stats, n_c, sh_q, &sh_n, &sh_base, &sh_peeled);
+}
+
 static size_t peel_smem(uint32_t k) { return (size_t)kPeelThreads * peel_q_per_thread(k) * sizeof(uint2); }
 
 template <int KT>
@@ -484,9 +561,9 @@ static int peel_grid(int dev, uint32_t k) {
 }
 
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
-                        const uint32_t* cand, float* dense, uint64_t cap, CellState* cells,
+                        const uint32_t* cand, float* dense, uint64_t cap, void* cells,
                         uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* out_val,
-                        uint8_t* out_peeled, lhc_stats* stats, int prebuilt, cudaStream_t s) {
+                        uint8_t* out_peeled, lhc_stats* stats, int mode, cudaStream_t s) {
 #ifdef LHC_DEBUG_SYNC
     if (getenv("LHC_DEBUG_SKIP_PEEL")) return cudaSuccess;
 #endif
@@ -496,7 +573,7 @@ cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* ta
     void* args[] = {(void*)&Pc,    (void*)&counters, (void*)&tabS,    (void*)&cand,
                     (void*)&dense, (void*)&cap,      (void*)&cells,   (void*)&claim,
                     (void*)&frontier, (void*)&ctrl,  (void*)&out_val, (void*)&out_peeled,
-                    (void*)&stats, (void*)&prebuilt};
+                    (void*)&stats, (void*)&mode};
     cudaError_t err;
     if (P.k == 3)
         err = cudaLaunchCooperativeKernel((const void*)k_peel<3>, dim3(peel_grid<3>(dev, 3)),

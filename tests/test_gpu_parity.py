@@ -206,7 +206,7 @@ def test_pipeline(lhc, ora, d, nnz, W, L, structure, law):
         assert np.array_equal(F(dec.dense), np.sum(np.stack(xs).astype(np.float64), axis=0))
 
 
-@pytest.mark.parametrize("build", ["rows", "insert"])
+@pytest.mark.parametrize("build", ["rows", "compact", "insert"])
 @pytest.mark.parametrize("d,nnz,W,L,structure", CASES)
 def test_cell_build_paths(lhc, ora, d, nnz, W, L, structure, build, monkeypatch):
     """Both ways of building the peeling state (per-candidate reductions, or by

@@ -153,15 +153,29 @@ class LosslessAllReduce:
 
     def step(self, xs, stream=None):
         """xs: list of dense fp32 device gradients of this rank's workers."""
+        return self._step([(x,) for x in xs], stream)
+
+    def step_coo(self, coos, stream=None):
+        """coos: list of (idx int32, val fp32) device COO gradients of this rank's
+        workers (sketch_compress_coo); same result as step() on the dense form."""
+        return self._step(list(coos), stream)
+
+    def _step(self, items, stream):
+        def compress(sk, item):
+            if len(item) == 1:
+                sk.compress(item[0], stream=stream)
+            else:
+                sk.compress_coo(item[0], item[1], stream=stream)
+
         if self.per_worker:
-            for sk, x in zip(self.worker_sketches, xs):
+            for sk, item in zip(self.worker_sketches, items):
                 sk.clear(stream)
-                sk.compress(x, stream=stream)
+                compress(sk, item)
             aggregate(self.p, self.worker_sketches, self.sketch, stream)
         else:
             self.sketch.clear(stream)
-            for x in xs:
-                self.sketch.compress(x, stream=stream)
+            for item in items:
+                compress(self.sketch, item)
         if self.comm is not None and self.comm.world > 1:
             self.comm.allreduce(stream)
         return self.decoder(self.sketch, stream)

@@ -113,6 +113,24 @@ def test_compress_dense(lhc, ora, d, nnz, W, L, structure, law):
     assert int(nnz_out.item()) == sum(int((x != 0).sum()) for x in xs)
 
 
+def test_step_coo_equals_step(lhc, ora):
+    """LosslessAllReduce.step_coo (COO boundary) == step (dense boundary) == oracle."""
+    d, nnz, W, L = 1_000_003, 10_000, 4, 1024
+    s = lhc.size_workload(d, nnz / d, W, L=L)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=0xC00)
+    xs = make_workers(d, nnz, W, 55, "dyadic")
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    coos = []
+    for x in xs:
+        idx = np.flatnonzero(x).astype(np.uint32)
+        coos.append((torch.from_numpy(idx.view(np.int32)).cuda(), torch.from_numpy(x[idx]).cuda()))
+    dec = run.step_coo(coos)
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(ora_params(ora, p), xs)
+    assert np.array_equal(U(run.sketch.bitmap), B)
+    compare_decode(ora, dec, ref, exact=True)
+
+
 def test_compress_coo(lhc, ora):
     d, L = 900_001, 512
     s = lhc.size_workload(d, 0.02, 1, L=L)

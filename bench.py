@@ -89,7 +89,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except FileNotFoundError:
             self.proc = None
             return
@@ -360,7 +360,6 @@ def main():
             graph.replay()
         barrier()
     clocks.start()
-    time.sleep(0.3)
     barrier()
     # (1) headline: K steps, device time per step from events around each step
     step_ms = []
@@ -390,13 +389,24 @@ def main():
     for ev in per_step:
         collect(ev)
     total_ms = sum(a.elapsed_time(b) for a, b in step_ms)
+
     barrier()
-    clocks.stop()
     ms = total_ms / args.steps
     t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_max = float(t_local.item())
+    # keep the GPU loaded with untimed steps for ~0.6 s so the clock sampler
+    # (nvidia-smi every 20 ms, started before the timed region) sees the step's
+    # steady state, not only the few ms of the timed region; the count is the
+    # same on every rank (the step holds collective barriers)
+    for _ in range(max(1, min(4000, int(600.0 / max(ms_max, 1e-3))))):
+        if graph is not None:
+            graph.replay()
+        else:
+            step(None, None)
+    barrier()
+    clocks.stop()
 
     stats = run.decoder.read_stats()
 

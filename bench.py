@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--fuse-local", action="store_true",
                     help="compress a rank's workers straight into one sketch (no per-worker sketches)")
     ap.add_argument("--comm", choices=["p2p", "nccl"], default="p2p")
+    ap.add_argument("--decode", choices=["replicated", "sharded"], default="replicated",
+                    help="replicated: all-reduce, every rank decodes all of d (the north "
+                         "star); sharded: per-shard sub-sketches, reduce-scatter, every rank "
+                         "decodes its shard, all-gather of the decoded lists (NEXT-2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -239,10 +243,23 @@ def main():
     xs = [torch.from_numpy(x).to(dev) for x in host]
 
     comm = None
-    if world > 1 and args.comm == "p2p":
-        comm = lhc.PeerComm(p)
-    run = lhc.LosslessAllReduce(p, cap, local_workers=len(xs), per_worker=not args.fuse_local,
-                                comm=comm, device=dev)
+    sharded = args.decode == "sharded"
+    if sharded:
+        from paper_2402_07529_b200.sizing import shard_plan
+
+        if args.comm != "p2p":
+            raise SystemExit("--decode sharded uses the NVLink P2P reduce-scatter")
+        plan = shard_plan(wl.d, world, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb)
+        run = lhc.ShardedAllReduce(plan, seed=SEED, local_workers=len(xs),
+                                   per_worker=not args.fuse_local, device=dev)
+        p_dec = run.ps[rank]           # the shard this rank decodes
+        G = plan.shards
+    else:
+        if world > 1 and args.comm == "p2p":
+            comm = lhc.PeerComm(p)
+        run = lhc.LosslessAllReduce(p, cap, local_workers=len(xs),
+                                    per_worker=not args.fuse_local, comm=comm, device=dev)
+        p_dec = p
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -275,9 +292,12 @@ def main():
                 launches[0] += lhc.last_launch_count()
 
         mark("start")
+        if sharded:
+            return sharded_step(mark, cnt)
         if run.per_worker:
             for sk, x in zip(run.worker_sketches, xs):
                 sk.clear()
+                cnt()
                 mark("compress0")
                 sk.compress(x)
                 cnt()
@@ -287,6 +307,7 @@ def main():
             mark("aggregate")
         else:
             run.sketch.clear()
+            cnt()
             for x in xs:
                 mark("compress0")
                 run.sketch.compress(x)
@@ -308,6 +329,51 @@ def main():
         cnt()
         mark("peel")
 
+    def sharded_step(mark, cnt):
+        if run.per_worker:
+            for bufs, x in zip(run.worker_bufs, xs):
+                for sk in bufs:
+                    sk.clear()
+                    cnt()
+                mark("compress0")
+                for q, sk in enumerate(bufs):
+                    sk.compress(run.shard_input(x, q))
+                    cnt()
+                mark("compress1")
+            for q in range(G):
+                lhc.sketch_aggregate(run.ps[q], [b[q].bitmap for b in run.worker_bufs],
+                                     [b[q].counters for b in run.worker_bufs],
+                                     run.slots[q].bitmap, run.slots[q].counters)
+                cnt()
+            mark("aggregate")
+        else:
+            for sk in run.slots:
+                sk.clear()
+                cnt()
+            for x in xs:
+                mark("compress0")
+                for q, sk in enumerate(run.slots):
+                    sk.compress(run.shard_input(x, q))
+                    cnt()
+                mark("compress1")
+            mark("aggregate")
+        if world > 1:
+            lhc.sketch_reduce_scatter(run.handle)
+            cnt()
+        mark("allreduce")
+        dec = run.decoder
+        dec.query(run.slots[rank])
+        cnt()
+        mark("query")
+        dec.peel(run.slots[rank])
+        cnt()
+        mark("peel")
+        if world > 1:
+            lhc.sketch_allgather_decoded(run.handle, dec.idx, dec.val, dec.stats, run.plan.width,
+                                         wl.d, run.dense)
+            cnt()
+        mark("allgather")
+
     def barrier():
         if world > 1:
             dist.barrier()
@@ -322,7 +388,8 @@ def main():
     trace('timed')
     # ---- timed region: K steps, per-step events, L2 flushed between steps ----
     clocks = ClockSampler(local_rank)
-    phase = {"compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "query": 0.0, "peel": 0.0}
+    phase = {"compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "query": 0.0, "peel": 0.0,
+             "allgather": 0.0}
     compress_launch_ms = []
     launches = [0]
     total_ms = 0.0
@@ -415,7 +482,8 @@ def main():
     e2e = None
     if not args.no_e2e:
         pinned = [torch.from_numpy(x).pin_memory() for x in host]
-        out_host = torch.empty(p.d, dtype=torch.float32).pin_memory()
+        out_host = torch.empty(wl.d, dtype=torch.float32).pin_memory()
+        out_dense = run.dense if sharded else run.decoder.dense
         dev_in = [torch.empty_like(x) for x in xs]
         h2d = sum(x.numel() * 4 for x in pinned)
         d2h = out_host.numel() * 4
@@ -424,7 +492,7 @@ def main():
             for h, d_ in zip(pinned, dev_in):
                 d_.copy_(h, non_blocking=True)
             run.step(dev_in)
-            out_host.copy_(run.decoder.dense, non_blocking=True)
+            out_host.copy_(out_dense, non_blocking=True)
 
         for _ in range(2):
             e2e_step()
@@ -443,7 +511,7 @@ def main():
         e2e = {"value": wl.d / (float(e_ms.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": float(e_ms.item()),
-               "path": "pinned host x_w -> H2D -> LosslessAllReduce.step -> dense sum D2H"}
+               "path": f"pinned host x_w -> H2D -> {type(run).__name__}.step -> dense sum D2H"}
         if not np.isfinite(e2e["value"]):
             e2e = None
 
@@ -451,10 +519,14 @@ def main():
         # (idx, val) per worker -> H2D -> LosslessAllReduce.step_coo -> the aggregate's
         # candidate list (idx, val) and stats D2H (cap entries, no host sync inside)
         coo_host = [wl.coo(w) for w in my_workers]
+        if sharded:   # per-shard lists with shard-relative indices (split once on the host)
+            coo_host = [c for i, v in coo_host for c in run.split_coo(i, v)]
         pin_i = [torch.from_numpy(i.view(np.int32)).pin_memory() for i, _ in coo_host]
         pin_v = [torch.from_numpy(v).pin_memory() for _, v in coo_host]
         dev_i = [torch.empty_like(t, device=dev) for t in pin_i]
         dev_v = [torch.empty_like(t, device=dev) for t in pin_v]
+        pairs = list(zip(dev_i, dev_v))
+        items = [pairs[w * G:(w + 1) * G] for w in range(len(my_workers))] if sharded else pairs
         cap_ = run.decoder.cap
         oi = torch.empty(cap_, dtype=torch.int32).pin_memory()
         ov = torch.empty(cap_, dtype=torch.float32).pin_memory()
@@ -463,7 +535,7 @@ def main():
         def e2e_coo_step():
             for a, b in zip(pin_i + pin_v, dev_i + dev_v):
                 b.copy_(a, non_blocking=True)
-            d = run.step_coo(list(zip(dev_i, dev_v)))
+            d = run.step_coo(items)
             oi.copy_(d.idx[:cap_], non_blocking=True)
             ov.copy_(d.val[:cap_], non_blocking=True)
             ost.copy_(d.stats, non_blocking=True)
@@ -486,7 +558,9 @@ def main():
                "h2d_bytes_per_step": sum(t.numel() * 4 for t in pin_i + pin_v),
                "d2h_bytes_per_step": 8 * cap_ + 32, "ms_per_step": float(c_ms.item()),
                "path": "pinned host COO (idx, val) per worker -> H2D -> "
-                       "LosslessAllReduce.step_coo -> candidate list (idx, val) + stats D2H",
+                       f"{type(run).__name__}.step_coo -> candidate list (idx, val) + stats D2H"
+                       + (" (own shard's list; every rank also holds the dense sum)"
+                          if sharded else ""),
                "dense": dense_e2e}
 
     trace('roofline')
@@ -505,16 +579,33 @@ def main():
     per_step_ms = {k: v / args.steps for k, v in phase.items()}
     avg_compress_ms = sum(compress_launch_ms) / max(1, len(compress_launch_ms))
     # algorithmic bytes per launch (Measurement) and launches per step
-    kern = {
-        "k_compress_dense": (4 * wl.d + S, W_loc, avg_compress_ms, hbm, "hbm"),
-        "k_aggregate": ((W_loc + 1) * S, 1 if run.per_worker else 0,
-                        per_step_ms["aggregate"], hbm, "hbm"),
-        "k_allreduce": (2 * (world - 1) / world * S, 1 if world > 1 else 0,
-                        per_step_ms["allreduce"], nvl, "nvlink"),
-        "k_query": (int(p.m) // 8 + 4 * n_c, 1, per_step_ms["query"], hbm, "hbm"),
-        # peel + finalize, and the dense output (zeroed, then the values at candidates)
-        "k_peel": (16 * int(p.c) + 9 * n_c + 4 * wl.d, 1, per_step_ms["peel"], hbm, "hbm"),
-    }
+    if sharded:
+        S_all = sum(int(q.m) // 8 + 4 * int(q.c) for q in run.ps)
+        kern = {
+            # a worker's gradient is compressed by G launches, one per shard
+            "k_compress_dense": ((4 * wl.d + S_all) / G, W_loc * G, avg_compress_ms / G, hbm, "hbm"),
+            "k_aggregate": ((W_loc + 1) * S_all / G, G if run.per_worker else 0,
+                            per_step_ms["aggregate"] / G, hbm, "hbm"),
+            "k_reduce_scatter": ((world - 1) / world * S_all, 1 if world > 1 else 0,
+                                 per_step_ms["allreduce"], nvl, "nvlink"),
+            "k_query": (int(p_dec.m) // 8 + 4 * n_c, 1, per_step_ms["query"], hbm, "hbm"),
+            "k_peel": (16 * int(p_dec.c) + 9 * n_c + 4 * int(p_dec.d), 1, per_step_ms["peel"],
+                       hbm, "hbm"),
+            # the own list to every peer (8 B per item)
+            "k_allgather_decoded": (8 * n_c * (world - 1), 1 if world > 1 else 0,
+                                    per_step_ms["allgather"], nvl, "nvlink"),
+        }
+    else:
+        kern = {
+            "k_compress_dense": (4 * wl.d + S, W_loc, avg_compress_ms, hbm, "hbm"),
+            "k_aggregate": ((W_loc + 1) * S, 1 if run.per_worker else 0,
+                            per_step_ms["aggregate"], hbm, "hbm"),
+            "k_allreduce": (2 * (world - 1) / world * S, 1 if world > 1 else 0,
+                            per_step_ms["allreduce"], nvl, "nvlink"),
+            "k_query": (int(p.m) // 8 + 4 * n_c, 1, per_step_ms["query"], hbm, "hbm"),
+            # peel + finalize, and the dense output (zeroed, then the values at candidates)
+            "k_peel": (16 * int(p.c) + 9 * n_c + 4 * wl.d, 1, per_step_ms["peel"], hbm, "hbm"),
+        }
     kernels = {}
     for name, (byts, nl, ms_l, peak, bound) in kern.items():
         if nl == 0 or ms_l <= 0:
@@ -550,7 +641,9 @@ def main():
                        "index": "bitmap" if kb == INDEX_BITMAP else "bloom",
                        "sketch_bytes": int(p.m) // 8 + 4 * int(p.c),
                        "per_worker_sketches": run.per_worker,
-                       "comm": ("p2p" if comm is not None else "nccl") if world > 1 else "none",
+                       "decode": args.decode,
+                       "comm": ("p2p" if comm is not None or sharded else "nccl")
+                       if world > 1 else "none",
                        "l2": "flushed (256 MB write) between timed steps, outside the events",
                        "cuda_graph": graph is not None,
                        "kernel_timing": "CUDA events between kernels in a second K-step pass "
@@ -567,6 +660,8 @@ def main():
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
+    if sharded:
+        run.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

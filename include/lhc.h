@@ -157,6 +157,41 @@ int lhc_comm_create(int rank, int world, const void* handles /*world*64 bytes, h
 int sketch_allreduce(lhc_comm* comm, void* stream);
 void lhc_comm_destroy(lhc_comm* comm);
 
+/* Sharded aggregation and decode (DESIGN.md NEXT-2).  The coordinates [0, d)
+ * are split into `world` contiguous shards of shard_width coordinates (a
+ * multiple of 1024; the last shard ragged, none empty); shard q is an
+ * independent sketch of x[q*shard_width ...] with its own params ps_q (equal m
+ * and c on every shard; d = the shard's width; for the exact bitmap index the
+ * last shard's m = ceil(d_q/L)*L).  Every rank's buffer holds `world` slots of
+ * slot_bytes; slot q = [bitmap of shard q | counters of shard q at
+ * counters_off].  lhc_shard_layout gives the sizes for the LARGEST shard's
+ * params ps and a per-shard item capacity cap_items (< 2^32); the buffer must
+ * be zero-initialised and 256-byte aligned.
+ *   sketch_reduce_scatter   slot `rank` of every rank becomes the OR / sum over
+ *       all ranks of their slot `rank` (counters summed in ascending rank
+ *       order); the other slots are left as they were.  One NVLink push of
+ *       (world-1)/world of the sketch per rank, one cross-rank barrier.
+ *   sketch_allgather_decoded  after the rank decoded its shard (sketch_query +
+ *       sketch_peel on slot `rank`, out_dense = dense + rank*shard_width):
+ *       idx[n]/val[n] with n = *n_items (device; e.g. &stats->n_cand, clamped to
+ *       cap_items) are pushed to every peer, and every other shard's range of
+ *       dense[d] is overwritten with exactly the values its owner decoded
+ *       (0 elsewhere).  Every rank ends with the identical dense sum.
+ * A sharded communicator is created by lhc_shard_comm_create (same handle
+ * exchange as lhc_comm_create) and released by lhc_comm_destroy; calling
+ * sketch_allreduce on it, or the sharded calls on a plain one, is LHC_EINVAL.
+ * All ranks must issue the same sequence of calls. */
+int lhc_shard_layout(const lhc_params* ps, int world, uint64_t cap_items, size_t* slot_bytes,
+                     size_t* counters_off, size_t* total_bytes);
+int lhc_shard_comm_create(int rank, int world, const void* handles /*world*64 bytes, host*/,
+                          const uint64_t* offsets /*world, host*/, void* local_buf,
+                          size_t buf_bytes, const lhc_params* ps, uint64_t cap_items,
+                          lhc_comm** out);
+int sketch_reduce_scatter(lhc_comm* comm, void* stream);
+int sketch_allgather_decoded(lhc_comm* comm, const uint32_t* idx, const float* val,
+                             const unsigned long long* n_items /*device*/, uint64_t shard_width,
+                             uint32_t d, float* dense, void* stream);
+
 /* ---- Phase II: recovery (Alg. 1) ----------------------------- */
 
 /* Decode an aggregated sketch [bitmap, counters] (not modified):

@@ -26,6 +26,17 @@ from ._lib import (  # noqa: F401
     sketch_peel,
     sketch_query,
     sketch_hash_rows,
+    lhc_shard_layout,
+    lhc_shard_comm_create,
+    sketch_reduce_scatter,
+    sketch_allgather_decoded,
 )
-from .pipeline import Decoder, LosslessAllReduce, PeerComm, Sketch, aggregate  # noqa: F401
-from .sizing import size_for, size_workload, union_support  # noqa: F401
+from .pipeline import (  # noqa: F401
+    Decoder,
+    LosslessAllReduce,
+    PeerComm,
+    ShardedAllReduce,
+    Sketch,
+    aggregate,
+)
+from .sizing import shard_plan, size_for, size_workload, union_support  # noqa: F401

@@ -78,7 +78,8 @@ EXPORTS = [
     "sketch_hash_rows", "sketch_clear", "sketch_compress", "sketch_compress_coo",
     "sketch_aggregate", "lhc_comm_layout", "lhc_ipc_handle", "lhc_comm_create",
     "sketch_allreduce", "lhc_comm_destroy", "sketch_decompress", "lhc_last_launch_count",
-    "sketch_query", "sketch_peel",
+    "sketch_query", "sketch_peel", "lhc_shard_layout", "lhc_shard_comm_create",
+    "sketch_reduce_scatter", "sketch_allgather_decoded",
 ]
 
 
@@ -112,6 +113,12 @@ def lib() -> ctypes.CDLL:
             "lhc_last_launch_count": (i32, []),
             "sketch_query": (i32, [P, vp, vp, sz, u64, vp, vp, vp]),
             "sketch_peel": (i32, [P, vp, vp, sz, u64, vp, vp, vp, vp, vp, vp]),
+            "lhc_shard_layout": (i32, [P, i32, u64, ctypes.POINTER(sz), ctypes.POINTER(sz),
+                                       ctypes.POINTER(sz)]),
+            "lhc_shard_comm_create": (i32, [i32, i32, vp, vp, vp, sz, P, u64,
+                                            ctypes.POINTER(vp)]),
+            "sketch_reduce_scatter": (i32, [vp, vp]),
+            "sketch_allgather_decoded": (i32, [vp, vp, vp, vp, u64, u32, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -276,6 +283,38 @@ def lhc_comm_create(rank: int, world: int, handles: list[bytes], offsets: list[i
 
 def sketch_allreduce(comm: int, stream=None):
     _check("sketch_allreduce", lib().sketch_allreduce(comm, _stream(stream)))
+
+
+def lhc_shard_layout(ps: lhc_params, world: int, cap_items: int):
+    """(slot_bytes, counters_off, total_bytes) of a sharded communication buffer."""
+    vals = [ctypes.c_size_t() for _ in range(3)]
+    _check("lhc_shard_layout", lib().lhc_shard_layout(ctypes.byref(ps), int(world), int(cap_items),
+                                                      *[ctypes.byref(v) for v in vals]))
+    return tuple(int(v.value) for v in vals)
+
+
+def lhc_shard_comm_create(rank: int, world: int, handles: list[bytes], offsets: list[int],
+                          buf: torch.Tensor, ps: lhc_params, cap_items: int) -> int:
+    hb = ctypes.create_string_buffer(b"".join(handles), 64 * world)
+    ob = (ctypes.c_uint64 * world)(*offsets)
+    out = ctypes.c_void_p()
+    _check("lhc_shard_comm_create", lib().lhc_shard_comm_create(
+        rank, world, hb, ob, buf.data_ptr(), buf.numel() * buf.element_size(), ctypes.byref(ps),
+        int(cap_items), ctypes.byref(out)))
+    return out.value
+
+
+def sketch_reduce_scatter(comm: int, stream=None):
+    _check("sketch_reduce_scatter", lib().sketch_reduce_scatter(comm, _stream(stream)))
+
+
+def sketch_allgather_decoded(comm: int, idx: torch.Tensor, val: torch.Tensor, stats: torch.Tensor,
+                             shard_width: int, d: int, dense: torch.Tensor, stream=None):
+    """n_items is read on the device from stats.n_cand (lhc_stats offset 0)."""
+    _check("sketch_allgather_decoded", lib().sketch_allgather_decoded(
+        comm, _dev(idx, torch.int32, None, "idx"), _dev(val, torch.float32, None, "val"),
+        _dev(stats, torch.uint8, STATS_BYTES, "stats"), int(shard_width), int(d),
+        _dev(dense, torch.float32, d, "dense"), _stream(stream)))
 
 
 def lhc_comm_destroy(comm: int):

@@ -176,6 +176,163 @@ __global__ void __launch_bounds__(256) k_allreduce(ArArgs A) {
         *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot) = epoch + 2;
 }
 
+
+// ---------------------------------------------------------------------------
+// Sharded aggregation (DESIGN.md NEXT-2, sharded decode).  The coordinates are
+// split into G contiguous shards, shard q with its own sub-sketch; every rank's
+// buffer is
+//   [G slots of slot_units 16-byte units | staging: 2 x G slots | gather: 2 x G x
+//    cap items (uint2) | signals + gather counts]
+// slot q = [B_q | pad | Y_q], units [0, y_unit) combine with OR, the rest with +.
+// sketch_reduce_scatter: push slot q -> rank q's staging[par][rank]; one barrier;
+//   rank r reduces its slot r with the G-1 staged copies in ascending rank order.
+// sketch_allgather_decoded: push my decoded (idx, val) list -> every peer's
+//   gather[par][rank] (+ count); zero the peer-shard ranges of the local dense
+//   output; one barrier; scatter every peer's list into them.
+// Staging and gather areas alternate by call parity (per-op counters in the
+// signal area), so one barrier per call suffices: a rank pushing in call k+1
+// has passed call k's barrier, which every peer reached only after finishing
+// call k-1, the last reader of the same-parity buffers.
+// ---------------------------------------------------------------------------
+constexpr int kRsCountSlot = 33;
+constexpr int kAgCountSlot = 34;
+constexpr int kGatherCountSlot = 64;  // u32 [2][kMaxRanks] from here
+
+struct ShArgs {
+    uint4* slots[kMaxRanks];  // slot region of every rank
+    uint4* stage[kMaxRanks];  // staging region of every rank: [2][G][slot_units]
+    uint2* gather[kMaxRanks]; // gather region of every rank: [2][G][cap]
+    uint32_t* sig[kMaxRanks];
+    uint64_t slot_units, y_unit, cap;
+    int rank, world;
+    // all-gather only
+    const uint32_t* idx;
+    const float* val;
+    const unsigned long long* n_items;
+    float* dense;
+    uint64_t shard_width;
+    uint32_t d;
+};
+
+template <int G>
+__device__ void sh_barrier(cg::grid_group& grid, const ShArgs& A, uint32_t epoch) {
+    ArArgs B{};
+    for (int q = 0; q < G; q++) B.sig[q] = A.sig[q];
+    B.rank = A.rank;
+    B.world = G;
+    xrank_barrier(grid, B, epoch);
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_reduce_scatter(ShArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t epoch = *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot);
+    const uint32_t par = *(volatile uint32_t*)(A.sig[A.rank] + kRsCountSlot) & 1u;
+    const uint64_t n = A.slot_units;
+#pragma unroll 1
+    for (int dd = 1; dd < G; dd++) {
+        const int q = (A.rank + dd) % G;
+        const uint4* src = A.slots[A.rank] + (uint64_t)q * n;
+        uint4* out = A.stage[q] + ((uint64_t)par * G + A.rank) * n;
+        for (uint64_t u0 = gtid; u0 < n; u0 += kU * gstride) {
+            uint4 v[kU];
+#pragma unroll
+            for (int a = 0; a < kU; a++)
+                if (u0 + a * gstride < n) v[a] = __ldcs(src + u0 + a * gstride);
+#pragma unroll
+            for (int a = 0; a < kU; a++)
+                if (u0 + a * gstride < n) out[u0 + a * gstride] = v[a];
+        }
+    }
+    sh_barrier<G>(grid, A, epoch + 1);
+    constexpr int U = G <= 2 ? 4 : G <= 4 ? 2 : 1;
+    uint4* mine = A.slots[A.rank] + (uint64_t)A.rank * n;
+    const uint4* st = A.stage[A.rank] + (uint64_t)par * G * n;
+    for (uint64_t u0 = gtid; u0 < n; u0 += U * gstride) {
+        uint4 v[U][G];
+#pragma unroll
+        for (int a = 0; a < U; a++) {
+            const uint64_t u = u0 + a * gstride;
+            if (u < n) {
+#pragma unroll
+                for (int r = 0; r < G; r++) v[a][r] = r == A.rank ? __ldcg(mine + u) : __ldcg(st + r * n + u);
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < U; a++) {
+            const uint64_t u = u0 + a * gstride;
+            if (u >= n) continue;
+            if (u < A.y_unit) {
+                uint4 acc = v[a][0];
+#pragma unroll
+                for (int r = 1; r < G; r++) combine(acc, v[a][r]);
+                mine[u] = acc;
+            } else {
+                float4 acc = *reinterpret_cast<float4*>(&v[a][0]);
+#pragma unroll
+                for (int r = 1; r < G; r++) combine(acc, *reinterpret_cast<float4*>(&v[a][r]));
+                mine[u] = *reinterpret_cast<uint4*>(&acc);
+            }
+        }
+    }
+    // every block read epoch / par before the barrier's grid syncs
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot) = epoch + 1;
+        *(volatile uint32_t*)(A.sig[A.rank] + kRsCountSlot) = par + 1;
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t epoch = *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot);
+    const uint32_t par = *(volatile uint32_t*)(A.sig[A.rank] + kAgCountSlot) & 1u;
+    const uint64_t n = min((uint64_t)*A.n_items, A.cap);
+    // push my list to every peer (value bits travel with the local index)
+#pragma unroll 1
+    for (int dd = 1; dd < G; dd++) {
+        const int q = (A.rank + dd) % G;
+        uint2* out = A.gather[q] + ((uint64_t)par * G + A.rank) * A.cap;
+        for (uint64_t i = gtid; i < n; i += gstride)
+            out[i] = make_uint2(__ldcg(A.idx + i), __float_as_uint(__ldcg(A.val + i)));
+        if (gtid == 0) A.sig[q][kGatherCountSlot + par * kMaxRanks + A.rank] = (uint32_t)n;
+    }
+    // zero the peers' shard ranges of the local dense output meanwhile
+    {
+        const uint64_t lo = (uint64_t)A.rank * A.shard_width;
+        const uint64_t hi = min((uint64_t)A.d, lo + A.shard_width);
+        float4* d4 = reinterpret_cast<float4*>(A.dense);
+        const uint64_t n4 = A.d / 4;  // shard_width is a multiple of 4
+        for (uint64_t u = gtid; u < n4; u += gstride)
+            if (4 * u < lo || 4 * u >= hi) __stcs(d4 + u, make_float4(0.f, 0.f, 0.f, 0.f));
+        for (uint64_t i = 4 * n4 + gtid; i < A.d; i += gstride)
+            if (i < lo || i >= hi) A.dense[i] = 0.f;
+    }
+    sh_barrier<G>(grid, A, epoch + 1);
+#pragma unroll 1
+    for (int dd = 1; dd < G; dd++) {
+        const int q = (A.rank + dd) % G;
+        const uint64_t nq = min((uint64_t)*(volatile uint32_t*)(A.sig[A.rank] + kGatherCountSlot +
+                                                               par * kMaxRanks + q),
+                                A.cap);
+        const uint2* in = A.gather[A.rank] + ((uint64_t)par * G + q) * A.cap;
+        float* base = A.dense + (uint64_t)q * A.shard_width;
+        for (uint64_t i = gtid; i < nq; i += gstride) {
+            const uint2 e = __ldcs(in + i);
+            if (e.y) base[e.x] = __uint_as_float(e.y);
+        }
+    }
+    // every block read epoch / par before the barrier's grid syncs
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot) = epoch + 1;
+        *(volatile uint32_t*)(A.sig[A.rank] + kAgCountSlot) = par + 1;
+    }
+}
+
 }  // namespace lhc
 
 struct lhc_comm {
@@ -186,6 +343,10 @@ struct lhc_comm {
     void* opened[lhc::kMaxRanks];
     size_t bitmap_off, counters_off, stage_b_off, stage_y_off, signals_off, total;
     int grid;
+    // sharded communicator (lhc_shard_comm_create)
+    int sharded;
+    uint64_t slot_bytes, y_off, cap;
+    size_t stage_off, gather_off;
 };
 
 using namespace lhc;
@@ -204,7 +365,73 @@ static void layout(const lhc_params* p, size_t* b, size_t* y, size_t* sb, size_t
     *t = *s + kSignalBytes;
 }
 
+// sharded buffer: [G slots | staging 2 x G slots | gather 2 x G x cap x 8 B | signals 512 B]
+static int shard_layout(const lhc_params* ps, int world, uint64_t cap, size_t* slot, size_t* y_off,
+                        size_t* stage, size_t* gather, size_t* sig, size_t* total) {
+    if (int rc = validate(ps)) return rc;
+    if (world < 1 || world > kMaxRanks) return set_error(LHC_EINVAL, "world must be in [1, 8]");
+    if (cap == 0 || cap >= (1ull << 32)) return set_error(LHC_EINVAL, "cap_items must be in [1, 2^32)");
+    *y_off = align_up(ps->m / 8, 256);
+    *slot = align_up(*y_off + ps->c * sizeof(float), 256);
+    *stage = *slot * world;
+    *gather = *stage + 2 * *slot * world;
+    *sig = align_up(*gather + 2 * (size_t)world * cap * 8, 256);
+    *total = *sig + 2 * kSignalBytes;
+    return LHC_OK;
+}
+
+static int shard_grid() {
+    const void* fns[] = {(const void*)k_reduce_scatter<2>, (const void*)k_reduce_scatter<3>,
+                         (const void*)k_reduce_scatter<4>, (const void*)k_reduce_scatter<5>,
+                         (const void*)k_reduce_scatter<6>, (const void*)k_reduce_scatter<7>,
+                         (const void*)k_reduce_scatter<8>, (const void*)k_allgather_decoded<2>,
+                         (const void*)k_allgather_decoded<3>, (const void*)k_allgather_decoded<4>,
+                         (const void*)k_allgather_decoded<5>, (const void*)k_allgather_decoded<6>,
+                         (const void*)k_allgather_decoded<7>, (const void*)k_allgather_decoded<8>};
+    int per_sm = 4;
+    for (const void* f : fns) {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, 256, 0);
+        per_sm = std::min(per_sm, n);
+    }
+    return std::max(1, per_sm) * num_sms();
+}
+
+static ShArgs shard_args(const lhc_comm* c) {
+    ShArgs A{};
+    for (int q = 0; q < c->world; q++) {
+        A.slots[q] = reinterpret_cast<uint4*>(c->peers[q]);
+        A.stage[q] = reinterpret_cast<uint4*>(c->peers[q] + c->stage_off);
+        A.gather[q] = reinterpret_cast<uint2*>(c->peers[q] + c->gather_off);
+        A.sig[q] = reinterpret_cast<uint32_t*>(c->peers[q] + c->signals_off);
+    }
+    A.slot_units = c->slot_bytes / 16;
+    A.y_unit = c->y_off / 16;
+    A.cap = c->cap;
+    A.rank = c->rank;
+    A.world = c->world;
+    return A;
+}
+
+static int launch_coop(const void* fn, const lhc_comm* c, ShArgs& A, void* stream, const char* what) {
+    void* args[] = {(void*)&A};
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(c->grid), dim3(256), args, 0, (cudaStream_t)stream);
+    count_launch();
+    if (e != cudaSuccess) return set_error(LHC_ECUDA, "%s launch: %s", what, cudaGetErrorString(e));
+    return LHC_OK;
+}
+
 extern "C" {
+
+int lhc_shard_layout(const lhc_params* ps, int world, uint64_t cap_items, size_t* slot_bytes,
+                     size_t* counters_off, size_t* total_bytes) {
+    size_t slot, y, st, ga, sg, t;
+    if (int rc = shard_layout(ps, world, cap_items, &slot, &y, &st, &ga, &sg, &t)) return rc;
+    if (slot_bytes) *slot_bytes = slot;
+    if (counters_off) *counters_off = y;
+    if (total_bytes) *total_bytes = t;
+    return LHC_OK;
+}
 
 int lhc_comm_layout(const lhc_params* p, size_t* bitmap_off, size_t* counters_off,
                     size_t* signals_off, size_t* total_bytes) {
@@ -296,6 +523,7 @@ int lhc_comm_create(int rank, int world, const void* handles, const uint64_t* of
 
 int sketch_allreduce(lhc_comm* c, void* stream) {
     if (!c) return set_error(LHC_EINVAL, "NULL comm");
+    if (c->sharded) return set_error(LHC_EINVAL, "sharded communicator: use sketch_reduce_scatter");
     reset_launches();
     if (c->world == 1) return LHC_OK;
     ArArgs A{};
@@ -329,6 +557,89 @@ int sketch_allreduce(lhc_comm* c, void* stream) {
     count_launch();
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "allreduce launch: %s", cudaGetErrorString(e));
     return LHC_OK;
+}
+
+int lhc_shard_comm_create(int rank, int world, const void* handles, const uint64_t* offsets,
+                          void* local_buf, size_t buf_bytes, const lhc_params* ps, uint64_t cap_items,
+                          lhc_comm** out) {
+    size_t slot, y, st, ga, sg, t;
+    if (int rc = shard_layout(ps, world, cap_items, &slot, &y, &st, &ga, &sg, &t)) return rc;
+    if (!out || !local_buf) return set_error(LHC_EINVAL, "NULL argument");
+    if (rank < 0 || rank >= world) return set_error(LHC_EINVAL, "0 <= rank < world required");
+    if (world > 1 && (!handles || !offsets)) return set_error(LHC_EINVAL, "NULL handles/offsets");
+    if (((uintptr_t)local_buf & 255u) != 0) return set_error(LHC_EINVAL, "buffer must be 256-byte aligned");
+    if (buf_bytes < t) return set_error(LHC_ECAPACITY, "shard buffer too small: %zu < %zu", buf_bytes, t);
+    lhc_comm* c = new lhc_comm();
+    c->rank = rank;
+    c->world = world;
+    c->p = *ps;
+    c->local = static_cast<char*>(local_buf);
+    c->sharded = 1;
+    c->slot_bytes = slot;
+    c->y_off = y;
+    c->cap = cap_items;
+    c->stage_off = st;
+    c->gather_off = ga;
+    c->signals_off = sg;
+    c->total = t;
+    for (int q = 0; q < world; q++) {
+        if (q == rank) {
+            c->peers[q] = c->local;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, static_cast<const char*>(handles) + 64 * q, 64);
+        void* ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            for (int a = 0; a < q; a++)
+                if (c->opened[a]) cudaIpcCloseMemHandle(c->opened[a]);
+            delete c;
+            return set_error(LHC_ECOMM, "cudaIpcOpenMemHandle(rank %d): %s", q, cudaGetErrorString(e));
+        }
+        c->opened[q] = ptr;
+        c->peers[q] = static_cast<char*>(ptr) + offsets[q];
+    }
+    c->grid = shard_grid();
+    *out = c;
+    return LHC_OK;
+}
+
+int sketch_reduce_scatter(lhc_comm* c, void* stream) {
+    if (!c || !c->sharded) return set_error(LHC_EINVAL, "not a sharded communicator");
+    reset_launches();
+    if (c->world == 1) return LHC_OK;
+    ShArgs A = shard_args(c);
+    const void* fns[kMaxRanks + 1] = {nullptr, nullptr,
+                                      (const void*)k_reduce_scatter<2>, (const void*)k_reduce_scatter<3>,
+                                      (const void*)k_reduce_scatter<4>, (const void*)k_reduce_scatter<5>,
+                                      (const void*)k_reduce_scatter<6>, (const void*)k_reduce_scatter<7>,
+                                      (const void*)k_reduce_scatter<8>};
+    return launch_coop(fns[c->world], c, A, stream, "reduce_scatter");
+}
+
+int sketch_allgather_decoded(lhc_comm* c, const uint32_t* idx, const float* val,
+                             const unsigned long long* n_items, uint64_t shard_width, uint32_t d,
+                             float* dense, void* stream) {
+    if (!c || !c->sharded) return set_error(LHC_EINVAL, "not a sharded communicator");
+    if (!idx || !val || !n_items || !dense) return set_error(LHC_EINVAL, "NULL argument");
+    if (shard_width == 0 || shard_width % 4 || (uint64_t)(c->world - 1) * shard_width >= d)
+        return set_error(LHC_EINVAL, "shard_width must be a positive multiple of 4, every shard non-empty");
+    reset_launches();
+    if (c->world == 1) return LHC_OK;
+    ShArgs A = shard_args(c);
+    A.idx = idx;
+    A.val = val;
+    A.n_items = n_items;
+    A.dense = dense;
+    A.shard_width = shard_width;
+    A.d = d;
+    const void* fns[kMaxRanks + 1] = {nullptr, nullptr,
+                                      (const void*)k_allgather_decoded<2>, (const void*)k_allgather_decoded<3>,
+                                      (const void*)k_allgather_decoded<4>, (const void*)k_allgather_decoded<5>,
+                                      (const void*)k_allgather_decoded<6>, (const void*)k_allgather_decoded<7>,
+                                      (const void*)k_allgather_decoded<8>};
+    return launch_coop(fns[c->world], c, A, stream, "allgather");
 }
 
 void lhc_comm_destroy(lhc_comm* c) {

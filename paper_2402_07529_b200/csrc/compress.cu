@@ -54,7 +54,7 @@ void launch_hash_rows(const KParams& P, uint32_t dom, uint64_t n_rows, uint2* ou
 // gradient does not evict the sketch lines they accumulate into.
 // ---------------------------------------------------------------------------
 #ifndef LHC_COMPRESS_WARPS
-#define LHC_COMPRESS_WARPS 8
+#define LHC_COMPRESS_WARPS 16
 #endif
 #ifndef LHC_COMPRESS_STAGES
 #define LHC_COMPRESS_STAGES 2

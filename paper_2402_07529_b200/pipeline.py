@@ -179,3 +179,145 @@ class LosslessAllReduce:
         if self.comm is not None and self.comm.world > 1:
             self.comm.allreduce(stream)
         return self.decoder(self.sketch, stream)
+
+
+class _SlotSketch:
+    """A Sketch-like view of slot q of a sharded buffer (bitmap and counters of one shard)."""
+
+    def __init__(self, p: L.lhc_params, buf: torch.Tensor, base: int, y_off: int):
+        self.p = p
+        self.bitmap = buf[base:base + p.words * 4].view(torch.int32)
+        self.counters = buf[base + y_off:base + y_off + int(p.c) * 4].view(torch.float32)
+
+    clear = Sketch.clear
+    compress = Sketch.compress
+    compress_coo = Sketch.compress_coo
+
+
+class ShardedAllReduce:
+    """Alg. 1 with a sharded decode (DESIGN.md NEXT-2): coordinate shard q has its
+    own sub-sketch; every rank compresses its workers into all shards, the NVLink
+    reduce-scatter leaves rank r with the aggregate of shard r, rank r decodes
+    only shard r, and an all-gather of the decoded (index, value) lists gives
+    every rank the identical dense sum.  Construction is collective; with one
+    rank (no group) every shard is decoded locally.
+
+    plan: sizing.ShardPlan with plan.shards == world size (or any shard count on
+    one process, which then decodes every shard itself)."""
+
+    def __init__(self, plan, k: int = 3, L_rows: int = 1024, seed: int = 0, cap_cand: int = 0,
+                 local_workers: int = 1, per_worker: bool = True, group=None, device=None):
+        import torch.distributed as dist
+
+        self.plan = plan
+        s = plan.sizing
+        distributed = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if distributed else 0
+        self.world = dist.get_world_size(group) if distributed else 1
+        if plan.shards != self.world and self.world != 1:
+            raise ValueError(f"plan has {plan.shards} shards, world size is {self.world}")
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        self.ps = [L.params(plan.shard_d(q), plan.shard_m(q), s.c, k, s.k_bloom, L_rows, seed)
+                   for q in range(plan.shards)]
+        self.cap = int(cap_cand) or int(1.25 * s.n_cand_expected) + 4096
+        self.cap = min(self.cap, plan.width)
+        self.slot_bytes, self.y_off, total = L.lhc_shard_layout(self.ps[0], self.world, self.cap)
+        self.buf = torch.zeros(total, dtype=torch.uint8, device=device)
+        self.slots = [_SlotSketch(self.ps[q], self.buf, q * self.slot_bytes, self.y_off)
+                      for q in range(plan.shards)]
+        self.per_worker = per_worker and local_workers > 1
+        self.worker_bufs = []
+        if self.per_worker:
+            for _ in range(local_workers):
+                b = torch.zeros(self.slot_bytes * plan.shards, dtype=torch.uint8, device=device)
+                self.worker_bufs.append(
+                    [_SlotSketch(self.ps[q], b, q * self.slot_bytes, self.y_off)
+                     for q in range(plan.shards)])
+        self.dense = torch.empty(plan.d, dtype=torch.float32, device=device)
+        # the shards this process decodes: its own, or all of them on one rank
+        self.owned = [self.rank] if self.world > 1 else list(range(plan.shards))
+        self.decoders = {}
+        for q in self.owned:
+            lo, hi = plan.bounds(q)
+            dec = Decoder(self.ps[q], self.cap, dense=False, device=device)
+            dec.dense = self.dense[lo:hi]
+            self.decoders[q] = dec
+        self.decoder = self.decoders[self.owned[0]]
+        self.handle = None
+        if self.world > 1:
+            torch.cuda.synchronize()
+            handle, offset = L.lhc_ipc_handle(self.buf)
+            handles, offsets = exchange_handles(handle, offset, group)
+            self.handle = L.lhc_shard_comm_create(self.rank, self.world, handles, offsets,
+                                                  self.buf, self.ps[0], self.cap)
+            dist.barrier(group=group)
+
+    def shard_input(self, x: torch.Tensor, q: int) -> torch.Tensor:
+        lo, hi = self.plan.bounds(q)
+        return x[lo:hi]
+
+    def step(self, xs, stream=None):
+        """xs: dense fp32 device gradients (length d) of this rank's workers."""
+        return self._step([(x,) for x in xs], stream)
+
+    def step_coo(self, coos, stream=None):
+        """coos: per local worker, a list of G (idx int32, val fp32) device COO
+        gradients, one per shard, indices relative to the shard's first coordinate
+        (split_coo); same result as step() on the dense form."""
+        return self._step([tuple(c) for c in coos], stream, coo=True)
+
+    def split_coo(self, idx, val):
+        """Host helper: split a sorted COO gradient (numpy) into per-shard lists with
+        shard-relative indices, for step_coo."""
+        import numpy as np
+
+        out = []
+        for q in range(self.plan.shards):
+            lo, hi = self.plan.bounds(q)
+            a, b = np.searchsorted(idx, [lo, hi])
+            out.append(((idx[a:b] - lo).astype(idx.dtype), val[a:b]))
+        return out
+
+    def _compress_all(self, slots, item, stream, coo=False):
+        for q, sk in enumerate(slots):
+            if coo:
+                sk.compress_coo(item[q][0], item[q][1], stream=stream)
+            else:
+                sk.compress(self.shard_input(item[0], q), stream=stream)
+
+    def _step(self, items, stream, coo=False):
+        G = self.plan.shards
+        if self.per_worker:
+            for bufs, item in zip(self.worker_bufs, items):
+                for sk in bufs:
+                    sk.clear(stream)
+                self._compress_all(bufs, item, stream, coo)
+            for q in range(G):
+                L.sketch_aggregate(self.ps[q], [b[q].bitmap for b in self.worker_bufs],
+                                   [b[q].counters for b in self.worker_bufs],
+                                   self.slots[q].bitmap, self.slots[q].counters, stream)
+        else:
+            for sk in self.slots:
+                sk.clear(stream)
+            for item in items:
+                self._compress_all(self.slots, item, stream, coo)
+        if self.world > 1:
+            L.sketch_reduce_scatter(self.handle, stream)
+        for q in self.owned:
+            self.decoders[q](self.slots[q], stream)
+        dec = self.decoder
+        if self.world > 1:
+            L.sketch_allgather_decoded(self.handle, dec.idx, dec.val, dec.stats, self.plan.width,
+                                       self.plan.d, self.dense, stream)
+        return dec
+
+    def close(self):
+        if self.handle:
+            L.lhc_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

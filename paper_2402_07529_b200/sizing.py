@@ -145,3 +145,42 @@ def paper_sizes(n: float, lam: float, C: int, gamma: float = GAMMA_PAPER):
     s1 = bloom_bits(n, eps)
     s2 = gamma * C * n * (1.0 + eps * lam)
     return s1, s2
+
+
+# ---- sharded decode (DESIGN.md NEXT-2) ----------------------------------------
+
+@dataclass
+class ShardPlan:
+    """Coordinates [0, d) split into `shards` contiguous ranges of `width`
+    coordinates (a multiple of 1024: whole compress tiles and whole rows); shard q
+    is an independent sketch of its range, sized for its share of the support."""
+    d: int
+    shards: int
+    width: int
+    sizing: Sizing           # of the largest (full-width) shard
+
+    def bounds(self, q: int) -> tuple[int, int]:
+        lo = q * self.width
+        return lo, min(self.d, lo + self.width)
+
+    def shard_d(self, q: int) -> int:
+        lo, hi = self.bounds(q)
+        return hi - lo
+
+    def shard_m(self, q: int) -> int:
+        """m of shard q: equal on every shard, except the exact bitmap index
+        (one bit per coordinate of the shard, whole rows)."""
+        s = self.sizing
+        if s.k_bloom == INDEX_BITMAP:
+            return (self.shard_d(q) + s.L - 1) // s.L * s.L
+        return s.m
+
+
+def shard_plan(d: int, shards: int, density: float, workers: int, **kw) -> ShardPlan:
+    if shards < 1:
+        raise ValueError("shards must be >= 1")
+    width = -(-d // shards)
+    width = -(-width // 1024) * 1024
+    if (shards - 1) * width >= d:
+        raise ValueError(f"d={d} is too small for {shards} non-empty shards of {width}")
+    return ShardPlan(d, shards, width, size_workload(width, density, workers, **kw))

@@ -20,15 +20,83 @@ import torch.distributed as dist  # noqa: E402
 from lhc_inputs import config  # noqa: E402
 
 
+def sharded(name, law, steps, rank, world, dev):
+    """NEXT-2: reduce-scatter of per-shard sub-sketches, decode of the own shard,
+    all-gather of the decoded lists.  Every rank checks its shard against the
+    oracle on that coordinate range; all ranks must hold identical dense sums."""
+    import paper_2402_07529_b200 as lhc
+    from paper_2402_07529_b200.sizing import shard_plan
+
+    wl = config(name, law=law)
+    if name == "tiny":
+        wl = config(name, law=law, workers=max(world, 2), d=20_000 * world)
+    plan = shard_plan(wl.d, world, wl.density, wl.workers)
+    mine = [w for w in range(wl.workers) if w % world == rank]
+    xs = [torch.from_numpy(wl.dense(w)).to(dev) for w in mine]
+    run = lhc.ShardedAllReduce(plan, seed=0x5BA4D, local_workers=len(xs), device=dev)
+    for _ in range(steps):
+        dec = run.step(xs)
+    torch.cuda.synchronize()
+    st = dec.read_stats()
+    n = st["n_cand"]
+    dense = run.dense.cpu().numpy()
+    digest = torch.tensor([zlib.crc32(dense.tobytes())], dtype=torch.int64, device=dev)
+    allg = [torch.zeros_like(digest) for _ in range(world)]
+    dist.all_gather(allg, digest)
+    ok = all(torch.equal(allg[0], a) for a in allg)
+    import oracle
+
+    lo, hi = plan.bounds(rank)
+    p = run.ps[rank]
+    op = oracle.params(p.d, p.m, p.c, p.k, p.k_bloom, p.L, p.seed)
+    xs_all = [wl.dense(w) for w in range(wl.workers)]
+    Bo, Yo, ref = oracle.pipeline(op, [x[lo:hi] for x in xs_all], dense=True)
+    B = run.slots[rank].bitmap.cpu().numpy().view(np.uint32)
+    Y = run.slots[rank].counters.cpu().numpy()
+    idx = dec.idx[:n].cpu().numpy().view(np.uint32)
+    val = dec.val[:n].cpu().numpy()
+    ok &= np.array_equal(B, Bo)
+    ok &= n == ref.stats.n_cand and np.array_equal(idx, ref.cand)
+    ok &= np.array_equal(dec.peeled[:n].cpu().numpy().astype(bool), ref.peeled)
+    ok &= st["rounds"] == ref.stats.rounds and st["success"] == ref.stats.success
+
+    def close(a, b):
+        if law == "dyadic":
+            return np.array_equal(a.astype(np.float64), b)
+        return bool(np.all(np.abs(a - b) <= 1e-7 + 1e-5 * np.abs(b)))
+
+    ok &= close(Y, Yo) and close(val, ref.val) and close(dense[lo:hi], ref.dense)
+    # the other shards: every rank holds what their owners decoded
+    total = np.sum(np.stack(xs_all).astype(np.float64), axis=0)
+    if law == "dyadic" and st["success"]:
+        ok &= np.array_equal(dense[lo:hi].astype(np.float64), total[lo:hi])
+    print(f"mgpu-sharded {name} world={world} rank={rank} n_cand={n} rounds={st['rounds']} "
+          f"ok={ok}", flush=True)
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    # rank 0 additionally checks the assembled dense sum of all shards (dyadic: exact)
+    if rank == 0 and law == "dyadic":
+        good = bool(np.array_equal(dense.astype(np.float64), total))
+        print(f"mgpu-sharded dense == exact sum: {good}", flush=True)
+        flag &= torch.tensor([1 if good else 0], device=dev)
+    run.close()
+    return flag.item() == 1
+
+
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "ncf"
     law = sys.argv[2] if len(sys.argv) > 2 else "dyadic"
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    mode = sys.argv[4] if len(sys.argv) > 4 else "replicated"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
+    if mode == "sharded":
+        ok = sharded(name, law, steps, rank, world, dev)
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
     import paper_2402_07529_b200 as lhc
 
     wl = config(name, law=law)

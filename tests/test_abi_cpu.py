@@ -127,3 +127,52 @@ def test_theory_pins(lhc):
     assert worst < 1.6
     # 1.23 x (1 - 0.304) = 85.6 %
     assert round(1.23 * (1 - 0.304), 3) == 0.856
+
+
+# ------------------------------------------------- sharded layout (host) --
+
+@pytest.mark.parametrize("d,G", [(32_000_000, 8), (32_000_000, 2), (10_000_000, 3), (7_000, 3)])
+def test_shard_plan_covers_d(lhc, d, G):
+    from paper_2402_07529_b200.sizing import INDEX_BITMAP, shard_plan
+
+    for kb in (0, INDEX_BITMAP):
+        plan = shard_plan(d, G, 0.01, 8, k_bloom=kb)
+        assert plan.width % 1024 == 0
+        spans = [plan.bounds(q) for q in range(G)]
+        assert spans[0][0] == 0 and spans[-1][1] == d
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))     # contiguous, disjoint
+        assert all(plan.shard_d(q) > 0 for q in range(G))
+        for q in range(G):
+            p = lhc.params(plan.shard_d(q), plan.shard_m(q), plan.sizing.c, 3, kb, 1024, 1)
+            assert lhc.lhc_validate(p), (q, p, lhc._lib.last_error())
+            assert plan.shard_m(q) <= plan.sizing.m               # fits the largest slot
+
+
+def test_shard_plan_rejects_empty_shards(lhc):
+    from paper_2402_07529_b200.sizing import shard_plan
+
+    with pytest.raises(ValueError):
+        shard_plan(3000, 4, 0.01, 8)     # width 1024: the fourth shard would be empty
+
+
+def test_shard_layout(lhc):
+    from paper_2402_07529_b200.sizing import shard_plan
+
+    plan = shard_plan(32_000_000, 8, 0.01, 8)
+    s = plan.sizing
+    # the G sub-sketches together are the size of the unsharded sketch (within rounding)
+    full = lhc.size_workload(32_000_000, 0.01, 8)
+    assert abs(8 * (s.m / 8 + 4 * s.c) - (full.m / 8 + 4 * full.c)) / (full.m / 8 + 4 * full.c) < 0.01
+    ps = lhc.params(plan.width, s.m, s.c, 3, 0, 1024, 1)
+    slot, y, total = lhc.lhc_shard_layout(ps, 8, 500_000)
+    assert y >= s.m // 8 and y % 256 == 0 and slot >= y + 4 * s.c and slot % 256 == 0
+    # slots + double-buffered staging + double-buffered gather lists + signals
+    assert total >= 3 * 8 * slot + 2 * 8 * 500_000 * 8 + 512
+    with pytest.raises(lhc.LhcError):
+        lhc.lhc_shard_layout(ps, 9, 500_000)
+    with pytest.raises(lhc.LhcError):
+        lhc.lhc_shard_layout(ps, 8, 0)
+    L = lhc.lib()
+    assert L.sketch_reduce_scatter(None, None) == lhc._lib.LHC_EINVAL
+    assert L.sketch_allgather_decoded(None, None, None, None, 4096, 10_000, None, None) == \
+        lhc._lib.LHC_EINVAL

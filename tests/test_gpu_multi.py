@@ -25,3 +25,16 @@ def test_p2p_allreduce_parity(world, name, law):
            os.path.join(ROOT, "tests", "mgpu_worker.py"), name, law]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name,law", [("tiny", "dyadic"), ("ncf", "dyadic"), ("ncf", "gauss")])
+def test_sharded_decode_parity(world, name, law):
+    """NEXT-2: reduce-scatter -> decode the own shard -> all-gather (tests/mgpu_worker.py)."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29534",
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), name, law, "3", "sharded"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

@@ -388,3 +388,35 @@ def test_vgg_gamma_sweep(lhc, ora, gamma):
     B, Y, ref = ora.pipeline(op, xs, dense=False)
     assert np.array_equal(U(run.sketch.bitmap), B)
     compare_decode(ora, dec, ref, exact=True)
+
+
+# ---------------------------------------- sharded layout, one process (NEXT-2) --
+
+@pytest.mark.parametrize("d,nnz,W,G,kb", [
+    (1_000_003, 10_000, 3, 4, 0),        # ragged last shard
+    (1_000_003, 10_000, 3, 3, 255),      # exact bitmap: the last shard has a smaller m
+    (300_000, 30_000, 2, 2, 0),
+])
+@pytest.mark.parametrize("law", ["dyadic", "gauss"])
+def test_sharded_single_process(lhc, ora, d, nnz, W, G, kb, law):
+    """Every shard is an independent sketch of its coordinate range: its
+    bitmap, counters and decode equal the oracle's on that range with the
+    shard's params, and the assembled dense output is the concatenation."""
+    from paper_2402_07529_b200.sizing import shard_plan
+
+    plan = shard_plan(d, G, nnz / d, W, k_bloom=kb)
+    run = lhc.ShardedAllReduce(plan, seed=0x5AD + d, cap_cand=plan.width, local_workers=W)
+    xs = make_workers(d, nnz, W, 7 + d % 5, law)
+    for _ in range(2):    # the second step reuses the cleared buffers
+        dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    dense = F(run.dense)
+    for q in range(G):
+        lo, hi = plan.bounds(q)
+        p = run.ps[q]
+        B, Y, ref = ora.pipeline(ora_params(ora, p), [x[lo:hi] for x in xs])
+        assert np.array_equal(U(run.slots[q].bitmap), B)
+        assert_values(F(run.slots[q].counters), Y, law == "dyadic")
+        compare_decode(ora, run.decoders[q], ref, law == "dyadic")
+        assert_values(dense[lo:hi], ref.dense, law == "dyadic")
+    assert dec is run.decoders[0]

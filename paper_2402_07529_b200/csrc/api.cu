@@ -264,12 +264,7 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
     if (out_dense && !aligned16(out_dense)) return set_error(LHC_EINVAL, "out_dense must be 16-byte aligned");
     if (cap_cand && (!out_idx || !out_val || !out_peeled)) return set_error(LHC_EINVAL, "NULL output");
     cudaStream_t s = (cudaStream_t)stream;
-    float* dense = out_dense ? out_dense : v.dense;
-    if (cudaMemsetAsync(dense, 0, (size_t)p->d * sizeof(float), s) != cudaSuccess)
-        return check_launch("memset");
-    if (cudaMemsetAsync(v.dst_off, 0, ((p->c >> v.P.log2L) + 1) * sizeof(uint32_t), s) != cudaSuccess ||
-        cudaMemsetAsync(v.claim, 0, ((size_t)p->d + 31) / 32 * sizeof(uint32_t), s) != cudaSuccess)
-        return check_launch("memset");
+    float* dense = out_dense ? out_dense : v.dense;  // zeroed by the peel kernel
     // cell state larger than half the L2: build it by destination row (no random
     // HBM reductions), compact (8 B/cell) when the input rows fit in 22 bits;
     // otherwise the in-kernel per-candidate insert is faster.

@@ -26,8 +26,9 @@
 //            exactly those of synchronous peeling.
 //   finalize unpeeled candidates take the median over j of sign_j * R;
 //            the candidate list's values are gathered from the dense output.
-// The dense output is zeroed (stream-ordered memset) before the kernel, so every
-// non-candidate coordinate is exactly 0 without a separate densify pass.
+// The dense output and the claim bits are zeroed inside the kernel before the
+// rounds (in build mode 0 while the key reductions drain), so every
+// non-candidate coordinate is exactly 0 without a memset or a densify pass.
 // Queue appends are aggregated per CTA in shared memory (one global atomic per
 // CTA per pass); every cell enters the queue at most once (c entries).
 #include <cooperative_groups.h>
@@ -111,6 +112,49 @@ __device__ __forceinline__ float ld_cg_f32(const float* p) {
     float v;
     asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
     return v;
+}
+
+// L2 eviction-priority hints (LHC_PEEL_HINTS): the decode state is reused every
+// round, the dense output is written once per coordinate.
+#ifndef LHC_PEEL_HINTS
+#define LHC_PEEL_HINTS 1
+#endif
+__device__ __forceinline__ uint64_t pol_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t pol_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_hint(float* a, float v, uint64_t pol) {
+    if (LHC_PEEL_HINTS)
+        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+    else
+        *a = v;
+}
+__device__ __forceinline__ void red_add_hint(float* a, float v, uint64_t pol) {
+    if (LHC_PEEL_HINTS)
+        asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+    else
+        atomicAdd(a, v);
+}
+__device__ __forceinline__ unsigned long long atom_add_hint(unsigned long long* a, unsigned long long v,
+                                                            uint64_t pol) {
+    if (!LHC_PEEL_HINTS) return atomicAdd(a, v);
+    unsigned long long old;
+    asm volatile("atom.global.add.L2::cache_hint.u64 %0, [%1], %2, %3;"
+                 : "=l"(old) : "l"(a), "l"(v), "l"(pol) : "memory");
+    return old;
+}
+__device__ __forceinline__ uint32_t atom_add_hint(uint32_t* a, uint32_t v, uint64_t pol) {
+    if (!LHC_PEEL_HINTS) return atomicAdd(a, v);
+    uint32_t old;
+    asm volatile("atom.global.add.L2::cache_hint.u32 %0, [%1], %2, %3;"
+                 : "=r"(old) : "l"(a), "r"(v), "l"(pol) : "memory");
+    return old;
 }
 
 // Block-aggregated append of the pairs in sh_q to the queue segment that starts
@@ -257,6 +301,7 @@ void launch_build_cells(const KParams& P, const float* counters, const uint2* ta
 #else
 #define DBG(name)
 #endif
+    cudaMemsetAsync(dst_off, 0, (nD + 1) * sizeof(uint32_t), s);
     k_pair_count<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos);
     DBG("pair_count");
     k_pair_scan<<<1, 1024, 0, s>>>(dst_off, (uint32_t)nD + 1);
@@ -303,6 +348,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
+    const uint64_t pl = pol_last(), pf = pol_first();
 
     // F0 ("round 0"): cells of degree one with their candidate, through rc[0]
     {
@@ -388,7 +434,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                         if (ev[j] == e) ge = map_sign(mp[j]);
                     }
                     const float val = ge * Re;
-                    dense[p] = val;  // the value lands at its coordinate
+                    st_hint(dense + p, val, pf);  // the value lands at its coordinate
                     atomicAdd(sh_peeled, 1u);
                     // all reductions first (independent), then the queue appends
                     const K dec = (K)0 - C::one(COMPACT ? i : p);
@@ -398,8 +444,8 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                         if (!KT && j >= k) break;
                         // the pure cell held only p: nothing reads its state again
                         if (ev[j] == e) continue;
-                        atomicAdd(&cells[ev[j]].R, -map_sign(mp[j]) * val);
-                        rest[j] = atomicAdd(&cells[ev[j]].key, dec) + dec;
+                        red_add_hint(&cells[ev[j]].R, -map_sign(mp[j]) * val, pl);
+                        rest[j] = atom_add_hint(&cells[ev[j]].key, dec, pl) + dec;
                     }
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
@@ -430,14 +476,31 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
     }
     if (timer) ctrl->t[kCtrlTimes - 1] = globaltimer();
 
-    // finalize: median estimate of unpeeled candidates
-    for (uint64_t s = gtid; s < n_c; s += gstride) {
-        const uint32_t p = __ldg(cand + s);
-        const bool pe = (__ldcg(claim + (p >> 5)) >> (p & 31)) & 1u;
+    // finalize: median estimate of unpeeled candidates; four slots per
+    // thread with their loads in flight together
+    for (uint64_t s0 = gtid; s0 < n_c; s0 += 4 * gstride) {
+        uint32_t pp[4], cw[4];
+        float dv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint64_t s = s0 + u * gstride;
+            pp[u] = s < n_c ? __ldg(cand + s) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            cw[u] = s0 + u * gstride < n_c ? __ldcg(claim + (pp[u] >> 5)) : 0u;
+            dv[u] = s0 + u * gstride < n_c ? __ldcg(dense + pp[u]) : 0.f;
+        }
+#pragma unroll 1
+        for (int u = 0; u < 4; u++) {
+        const uint64_t s = s0 + u * gstride;
+        if (s >= n_c) break;
+        const uint32_t p = pp[u];
+        const bool pe = (cw[u] >> (p & 31)) & 1u;
         out_peeled[s] = pe ? 1 : 0;
         float val;
         if (pe) {
-            val = __ldcg(dense + p);
+            val = dv[u];
         } else {
             float v[NJ];
             for (uint32_t j = 0; j < k; j++) {
@@ -455,6 +518,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
             dense[p] = val;
         }
         out_val[s] = val;
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         stats->n_peeled = n_peeled;
@@ -462,6 +526,14 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
         stats->success = (uint64_t)n_peeled == n_c ? 1 : 0;
         ctrl->rounds_dbg = rounds;
     }
+}
+
+// dense[0, d) = 0 with streaming 16-byte stores (dense is 16-byte aligned)
+__device__ __forceinline__ void zero_dense(float* dense, uint32_t d, uint64_t gtid, uint64_t gstride) {
+    float4* d4 = reinterpret_cast<float4*>(dense);
+    const uint64_t n4 = d / 4;
+    for (uint64_t u = gtid; u < n4; u += gstride) __stcs(d4 + u, make_float4(0.f, 0.f, 0.f, 0.f));
+    for (uint64_t i = 4 * n4 + gtid; i < d; i += gstride) dense[i] = 0.f;
 }
 
 // KT: compile-time k (3) or 0 for a run-time k <= kMaxK.  mode: 0 = build the wide
@@ -497,6 +569,9 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     if (timer) ctrl->t[0] = globaltimer();
     if (mode == 2 && *(volatile uint32_t*)&ctrl->compact_fail) mode = 0;  // uniform
     __syncthreads();
+    // claim bits cleared (ordered before the rounds by the grid barriers below)
+    for (uint64_t w = gtid; w < ((uint64_t)P.d + 31) / 32; w += gstride) __stcg(claim + w, 0u);
+    if (mode != 0) zero_dense(dense, P.d, gtid, gstride);
 
     if (mode == 0) {
         CellState* cells = static_cast<CellState*>(cells_v);
@@ -534,6 +609,9 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                 atomicAdd(&cells[e2].key, (1ull << 32) + p);
             }
         }
+        // the dense output is zeroed while the reductions drain (fire-and-forget
+        // stores behind L2-bound atomics)
+        zero_dense(dense, P.d, gtid, gstride);
         grid.sync();
     }
     if (timer) ctrl->t[2] = globaltimer();

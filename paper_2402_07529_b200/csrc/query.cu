@@ -14,9 +14,9 @@
 // One cooperative kernel, one grid barrier:
 //   phase 1  candidate masks of every chunk -> gmask (d/8 bytes) and per-CTA
 //            totals; also the Count Sketch row-map table for the peel
-//   phase 2  CTA prefix = sum of the totals of the CTAs before it; then thread =
-//            word: a block scan of 256 word counts gives each word the slot of its
-//            first candidate and the thread writes them (ascending order).
+//   phase 2  CTA prefix = sum of the totals of the CTAs before it, warp prefix =
+//            + the totals of the warps before it; each warp expands its masks into
+//            the ascending candidate list (below).
 #include <cooperative_groups.h>
 
 #include "launch.h"
@@ -29,18 +29,6 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kQueryThreads = 256;  // 8 warps
 constexpr int kQueryWarps = kQueryThreads / 32;
 constexpr int kChunksPerWarp = 4;
-constexpr uint32_t kStage = 12288;  // staged candidates per block of 1024 words (48 KB)
-
-__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t lane, uint32_t* total) {
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, x, o);
-        if (lane >= (uint32_t)o) x += y;
-    }
-    *total = __shfl_sync(kFull, x, 31);
-    return x - v;
-}
 
 // Candidate masks of kChunksPerWarp chunks (lane = word); all lanes must call.
 // KB: compile-time number of Bloom probes (3) or 0 for a run-time k_bloom <= kMaxK.
@@ -144,11 +132,15 @@ __device__ __forceinline__ void query_chunks8_onerow(const KParams& P,
     }
 }
 
-// Phase 1 works on chunks (warp = chunk, lane = word), phase 2 on words (thread =
-// word): a block-wide scan of 256 word counts gives every word the slot of its
-// first candidate, and each thread writes its word's candidates.
+// Each warp owns a contiguous sub-range of its CTA's chunks.  Phase 1 works on
+// chunks (lane = word) and records the warp's candidate total; phase 2 walks the
+// same sub-range 128 words at a time (four coalesced rows of 32 words, lane =
+// word): a warp scan of the word popcounts gives every word its first slot and
+// the nonzero words are expanded one at a time by the whole warp (lane = bit), so
+// the candidates leave in ascending order with coalesced stores and no lane
+// serialises over a dense word.
 #ifndef LHC_QUERY_MINB
-#define LHC_QUERY_MINB 1
+#define LHC_QUERY_MINB 3
 #endif
 template <int KB>
 __global__ void __launch_bounds__(kQueryThreads, LHC_QUERY_MINB)
@@ -156,13 +148,14 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
         uint32_t* __restrict__ gmask, uint32_t* __restrict__ cta_total, uint64_t cap,
         uint32_t* __restrict__ out_idx, Ctrl* ctrl, lhc_stats* stats) {
     cg::grid_group grid = cg::this_grid();
-    extern __shared__ uint32_t sh_stage[];  // kStage candidates
     __shared__ uint32_t sh_warp[kQueryWarps];
     __shared__ unsigned long long sh_prefix;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
     const uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;  // chunks per CTA
     const uint64_t c_begin = min(nchunks, blockIdx.x * per), c_end = min(nchunks, c_begin + per);
+    const uint64_t wper = (c_end - c_begin + kQueryWarps - 1) / kQueryWarps;  // chunks per warp
+    const uint64_t wc_begin = min(c_end, c_begin + warp * wper), wc_end = min(c_end, wc_begin + wper);
 
     // Count Sketch row maps for the peel (grid-stride, independent of the query)
     {
@@ -174,27 +167,26 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
         }
     }
 
-    // phase 1: masks of this CTA's chunks (warp w takes chunk groups w, w + 8, ...)
+    // phase 1: masks of this warp's chunks
     uint32_t my_cnt = 0;
     if (KB != 0 && P.L == 1024) {
-        for (uint64_t c0 = c_begin + 8 * warp; c0 < c_end; c0 += 8 * kQueryWarps) {
+        for (uint64_t c0 = wc_begin; c0 < wc_end; c0 += 8) {
             uint32_t m[8];
-            query_chunks8_onerow<KB ? KB : 1>(P, bitmap, c0, c_end, lane, m);
+            query_chunks8_onerow<KB ? KB : 1>(P, bitmap, c0, wc_end, lane, m);
 #pragma unroll
             for (int cb = 0; cb < 8; cb++)
-                if (c0 + cb < c_end) {
+                if (c0 + cb < wc_end) {
                     gmask[(c0 + cb) * 32 + lane] = m[cb];
                     my_cnt += __popc(m[cb]);
                 }
         }
     } else {
-        for (uint64_t c0 = c_begin + kChunksPerWarp * warp; c0 < c_end;
-             c0 += kChunksPerWarp * kQueryWarps) {
+        for (uint64_t c0 = wc_begin; c0 < wc_end; c0 += kChunksPerWarp) {
             uint32_t m[kChunksPerWarp];
             query_chunks<KB>(P, bitmap, c0, lane, m);
 #pragma unroll
             for (int it = 0; it < kChunksPerWarp; it++)
-                if (c0 + it < c_end) {
+                if (c0 + it < wc_end) {
                     gmask[(c0 + it) * 32 + lane] = m[it];
                     my_cnt += __popc(m[it]);
                 }
@@ -215,56 +207,60 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
         unsigned long long acc = 0;
         for (uint32_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) acc += __ldcg(cta_total + b);
         for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-        __syncthreads();
         if (threadIdx.x == 0) sh_prefix = 0;
         __syncthreads();
         if (lane == 0 && acc) atomicAdd(&sh_prefix, acc);
         __syncthreads();
     }
     unsigned long long run = sh_prefix;
-    // blocks of 4 words per thread (16-byte loads); the candidates of a block are
-    // staged in shared memory (thread-serial over its bits) and copied out with
-    // coalesced stores, unless the block is denser than the staging buffer
-    const uint64_t w_begin = c_begin * 32, w_end = c_end * 32;  // multiples of 4
-    for (uint64_t w0 = w_begin; w0 < w_end; w0 += 4 * kQueryThreads) {
-        const uint64_t w = w0 + 4 * threadIdx.x;
-        uint4 m4 = make_uint4(0u, 0u, 0u, 0u);
-        if (w < w_end) m4 = __ldcg(reinterpret_cast<const uint4*>(gmask + w));
-        const uint32_t c0 = __popc(m4.x), c1 = __popc(m4.y), c2 = __popc(m4.z), c3 = __popc(m4.w);
-        uint32_t wt;
-        const uint32_t ex = warp_excl_scan(c0 + c1 + c2 + c3, lane, &wt);
-        __syncthreads();  // previous block's sh_warp / sh_stage readers are done
-        if (lane == 0) sh_warp[warp] = wt;
-        __syncthreads();
-        uint32_t before = 0, all = 0;
+    for (uint32_t v = 0; v < warp; v++) run += sh_warp[v];
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint64_t w_begin = wc_begin * 32, w_end = wc_end * 32;
+    for (uint64_t w0 = w_begin; w0 < w_end; w0 += 128) {
+        uint32_t m[4];
 #pragma unroll
-        for (int v = 0; v < kQueryWarps; v++) {
-            const uint32_t x = sh_warp[v];
-            before += (uint32_t)v < warp ? x : 0u;
-            all += x;
+        for (int r = 0; r < 4; r++) {
+            const uint64_t w = w0 + 32 * r + lane;
+            m[r] = w < w_end ? __ldcg(gmask + w) : 0u;
         }
-        const uint32_t q0 = (uint32_t)(w << 5);
-        const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
-        if (all <= kStage) {
-            uint32_t pos = before + ex;
 #pragma unroll
-            for (int k4 = 0; k4 < 4; k4++)
-                for (uint32_t mm = mw[k4]; mm; mm &= mm - 1)
-                    sh_stage[pos++] = q0 + 32 * k4 + (__ffs(mm) - 1);
-            __syncthreads();
-            for (uint32_t a = threadIdx.x; a < all; a += kQueryThreads)
-                if (run + a < cap) out_idx[run + a] = sh_stage[a];
-        } else {
-            unsigned long long pos = run + before + ex;
+        for (int r = 0; r < 4; r++) {
+            const uint32_t c = __popc(m[r]);
+            uint32_t x = c;  // inclusive warp scan
 #pragma unroll
-            for (int k4 = 0; k4 < 4; k4++)
-                for (uint32_t mm = mw[k4]; mm; mm &= mm - 1, pos++)
-                    if (pos < cap) out_idx[pos] = q0 + 32 * k4 + (__ffs(mm) - 1);
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            const uint32_t total = __shfl_sync(kFull, x, 31);
+            const uint32_t ex = x - c;
+            const uint32_t q0 = (uint32_t)((w0 + 32 * r) << 5);
+            const uint32_t nzw = __ballot_sync(kFull, m[r] != 0u);
+            const uint32_t maxc = __reduce_max_sync(kFull, c);
+            if (maxc <= (uint32_t)__popc(nzw)) {
+                // sparse words: every lane walks its own word (at most maxc steps)
+                unsigned long long pos = run + ex;
+                for (uint32_t mm = m[r]; mm; mm &= mm - 1, pos++)
+                    if (pos < cap) out_idx[pos] = q0 + 32 * lane + (__ffs(mm) - 1);
+            } else {
+                // dense words: the warp expands one word at a time (lane = bit)
+                for (uint32_t nz = nzw; nz; nz &= nz - 1) {
+                    const uint32_t wz = __ffs(nz) - 1;
+                    const uint32_t mw = __shfl_sync(kFull, m[r], wz);
+                    const uint32_t off = __shfl_sync(kFull, ex, wz);
+                    if ((mw >> lane) & 1u) {
+                        const unsigned long long pos = run + off + __popc(mw & lt);
+                        if (pos < cap) out_idx[pos] = q0 + 32 * wz + lane;
+                    }
+                }
+            }
+            run += total;
         }
-        run += all;
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-        const unsigned long long total = run;
+    // the last warp of the last CTA ends at the grand total
+    if (blockIdx.x == gridDim.x - 1 && warp == kQueryWarps - 1 && lane == 0) {
+        unsigned long long total = sh_prefix;
+        for (uint32_t v = 0; v < kQueryWarps; v++) total += sh_warp[v];
         ctrl->n_cand = total;
         ctrl->overflow = total > cap ? 1u : 0u;
         stats->n_cand = total;
@@ -276,11 +272,8 @@ template <int KB>
 static int query_grid(int dev) {
     static int cached[64] = {0};
     if (dev < 64 && cached[dev]) return cached[dev];
-    cudaFuncSetAttribute(k_query<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(kStage * sizeof(uint32_t)));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<KB>, kQueryThreads,
-                                                  kStage * sizeof(uint32_t));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<KB>, kQueryThreads, 0);
     int g = std::max(1, per_sm) * num_sms();
     if (dev < 64) cached[dev] = g;
     return g;
@@ -303,9 +296,9 @@ cudaError_t launch_query(const KParams& P, const uint32_t* bitmap, uint2* tabS, 
                     (void*)&stats};
     cudaError_t e = P.kb == 3
         ? cudaLaunchCooperativeKernel((const void*)k_query<3>, dim3(query_grid<3>(dev)),
-                                      dim3(kQueryThreads), args, kStage * sizeof(uint32_t), s)
+                                      dim3(kQueryThreads), args, 0, s)
         : cudaLaunchCooperativeKernel((const void*)k_query<0>, dim3(query_grid<0>(dev)),
-                                      dim3(kQueryThreads), args, kStage * sizeof(uint32_t), s);
+                                      dim3(kQueryThreads), args, 0, s);
     count_launch();
     return e;
 }

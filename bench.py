@@ -294,26 +294,19 @@ def main():
         mark("start")
         if sharded:
             return sharded_step(mark, cnt)
+        # all local workers' gradients in one compress launch (sketch_compress_batch)
+        dst = run.worker_sketches if run.per_worker else [run.sketch] * len(xs)
+        clr = run.worker_sketches if run.per_worker else [run.sketch]
+        lhc.sketch_clear_batch(p, [t.bitmap for t in clr], [t.counters for t in clr])
+        cnt()
+        mark("compress0")
+        lhc.sketch_compress_batch(p, xs, [t.bitmap for t in dst], [t.counters for t in dst])
+        cnt()
+        mark("compress1")
         if run.per_worker:
-            for sk, x in zip(run.worker_sketches, xs):
-                sk.clear()
-                cnt()
-                mark("compress0")
-                sk.compress(x)
-                cnt()
-                mark("compress1")
             lhc.aggregate(p, run.worker_sketches, run.sketch)
             cnt()
-            mark("aggregate")
-        else:
-            run.sketch.clear()
-            cnt()
-            for x in xs:
-                mark("compress0")
-                run.sketch.compress(x)
-                cnt()
-                mark("compress1")
-            mark("aggregate")
+        mark("aggregate")
         if world > 1:
             if comm is not None:
                 comm.allreduce()
@@ -330,33 +323,25 @@ def main():
         mark("peel")
 
     def sharded_step(mark, cnt):
+        targets = run.worker_bufs if run.per_worker else [run.slots] * len(xs)
+        clr = [sk for bufs in (run.worker_bufs if run.per_worker else [run.slots]) for sk in bufs]
+        lhc.sketch_clear_batch(run.ps[0], [sk.bitmap for sk in clr], [sk.counters for sk in clr])
+        cnt()
+        mark("compress0")
+        # every (worker, shard) pair in one launch
+        pairs = [(run.shard_input(x, q), sk, run.plan.shard_d(q))
+                 for bufs, x in zip(targets, xs) for q, sk in enumerate(bufs)]
+        lhc.sketch_compress_batch(run.ps[0], [a for a, _, _ in pairs], [b.bitmap for _, b, _ in pairs],
+                                  [b.counters for _, b, _ in pairs], ds=[c for _, _, c in pairs])
+        cnt()
+        mark("compress1")
         if run.per_worker:
-            for bufs, x in zip(run.worker_bufs, xs):
-                for sk in bufs:
-                    sk.clear()
-                    cnt()
-                mark("compress0")
-                for q, sk in enumerate(bufs):
-                    sk.compress(run.shard_input(x, q))
-                    cnt()
-                mark("compress1")
             for q in range(G):
                 lhc.sketch_aggregate(run.ps[q], [b[q].bitmap for b in run.worker_bufs],
                                      [b[q].counters for b in run.worker_bufs],
                                      run.slots[q].bitmap, run.slots[q].counters)
                 cnt()
-            mark("aggregate")
-        else:
-            for sk in run.slots:
-                sk.clear()
-                cnt()
-            for x in xs:
-                mark("compress0")
-                for q, sk in enumerate(run.slots):
-                    sk.compress(run.shard_input(x, q))
-                    cnt()
-                mark("compress1")
-            mark("aggregate")
+        mark("aggregate")
         if world > 1:
             lhc.sketch_reduce_scatter(run.handle)
             cnt()
@@ -582,8 +567,8 @@ def main():
     if sharded:
         S_all = sum(int(q.m) // 8 + 4 * int(q.c) for q in run.ps)
         kern = {
-            # a worker's gradient is compressed by G launches, one per shard
-            "k_compress_dense": ((4 * wl.d + S_all) / G, W_loc * G, avg_compress_ms / G, hbm, "hbm"),
+            # one launch: every local worker's gradient into its G shard sketches
+            "k_compress_dense": (W_loc * (4 * wl.d + S_all), 1, avg_compress_ms, hbm, "hbm"),
             "k_aggregate": ((W_loc + 1) * S_all / G, G if run.per_worker else 0,
                             per_step_ms["aggregate"] / G, hbm, "hbm"),
             "k_reduce_scatter": ((world - 1) / world * S_all, 1 if world > 1 else 0,
@@ -597,7 +582,8 @@ def main():
         }
     else:
         kern = {
-            "k_compress_dense": (4 * wl.d + S, W_loc, avg_compress_ms, hbm, "hbm"),
+            # one launch: every local worker's gradient into its sketch
+            "k_compress_dense": (W_loc * (4 * wl.d + S), 1, avg_compress_ms, hbm, "hbm"),
             "k_aggregate": ((W_loc + 1) * S, 1 if run.per_worker else 0,
                             per_step_ms["aggregate"], hbm, "hbm"),
             "k_allreduce": (2 * (world - 1) / world * S, 1 if world > 1 else 0,

@@ -109,6 +109,9 @@ int sketch_hash_rows(const lhc_params* p, uint32_t dom, uint64_t n_rows, uint32_
 
 /* Zero a sketch (bitmap: m/32 words, counters: c floats) before compression. */
 int sketch_clear(const lhc_params* p, uint32_t* bitmap, float* counters, void* stream);
+/* sketch_clear of n sketches in one launch (HOST arrays of n device pointers). */
+int sketch_clear_batch(const lhc_params* p, int n, uint32_t* const* bitmaps, float* const* counters,
+                       void* stream);
 
 /* Compress a dense fp32 gradient x[d] (Alg. 1 Phase I; Count Sketch P:L175,
  * Bloom filter P:L230, batched layout P:L262).  Every coordinate with
@@ -120,6 +123,17 @@ int sketch_clear(const lhc_params* p, uint32_t* bitmap, float* counters, void* s
  * (device, nullable) is incremented by the number of nonzeros. */
 int sketch_compress(const lhc_params* p, const float* x, uint32_t* bitmap, float* counters,
                     unsigned long long* nnz_out, void* stream);
+
+/* n dense gradients in one launch (per 16 inputs): input b, xs[b][ds[b]] with
+ * ds[b] <= p->d (ds NULL: every input has p->d coordinates), is accumulated into
+ * (bitmaps[b], counters[b]) with the hash functions of p — the same result as n
+ * sketch_compress calls.  Sketches may repeat (homomorphic accumulation);
+ * a shorter input is a coordinate shard sketched with its own row range (DESIGN.md
+ * NEXT-2).  xs, bitmaps, counters: HOST arrays of n device pointers, each 16-byte
+ * aligned; nnz_out (device, nullable) receives the total nonzero count. */
+int sketch_compress_batch(const lhc_params* p, int n, const float* const* xs, const uint32_t* ds,
+                          uint32_t* const* bitmaps, float* const* counters,
+                          unsigned long long* nnz_out, void* stream);
 
 /* Same from a COO gradient: idx[nnz] (each < d, distinct), val[nnz].  Every
  * listed entry is inserted, including val == 0 (the index describes the listed
@@ -176,7 +190,8 @@ void lhc_comm_destroy(lhc_comm* comm);
  *       idx[n]/val[n] with n = *n_items (device; e.g. &stats->n_cand, clamped to
  *       cap_items) are pushed to every peer, and every other shard's range of
  *       dense[d] is overwritten with exactly the values its owner decoded
- *       (0 elsewhere).  Every rank ends with the identical dense sum.
+ *       (0 elsewhere).  Every rank ends with the identical dense sum.  idx, val
+ *       and dense must be 16-byte aligned.
  * A sharded communicator is created by lhc_shard_comm_create (same handle
  * exchange as lhc_comm_create) and released by lhc_comm_destroy; calling
  * sketch_allreduce on it, or the sharded calls on a plain one, is LHC_EINVAL.

@@ -30,6 +30,8 @@ from ._lib import (  # noqa: F401
     lhc_shard_comm_create,
     sketch_reduce_scatter,
     sketch_allgather_decoded,
+    sketch_clear_batch,
+    sketch_compress_batch,
 )
 from .pipeline import (  # noqa: F401
     Decoder,

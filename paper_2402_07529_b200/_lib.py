@@ -79,7 +79,8 @@ EXPORTS = [
     "sketch_aggregate", "lhc_comm_layout", "lhc_ipc_handle", "lhc_comm_create",
     "sketch_allreduce", "lhc_comm_destroy", "sketch_decompress", "lhc_last_launch_count",
     "sketch_query", "sketch_peel", "lhc_shard_layout", "lhc_shard_comm_create",
-    "sketch_reduce_scatter", "sketch_allgather_decoded",
+    "sketch_reduce_scatter", "sketch_allgather_decoded", "sketch_compress_batch",
+    "sketch_clear_batch",
 ]
 
 
@@ -119,6 +120,8 @@ def lib() -> ctypes.CDLL:
                                             ctypes.POINTER(vp)]),
             "sketch_reduce_scatter": (i32, [vp, vp]),
             "sketch_allgather_decoded": (i32, [vp, vp, vp, vp, u64, u32, vp, vp]),
+            "sketch_compress_batch": (i32, [P, i32, vp, vp, vp, vp, vp, vp]),
+            "sketch_clear_batch": (i32, [P, i32, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -197,6 +200,36 @@ def sketch_compress(p: lhc_params, x: torch.Tensor, bitmap: torch.Tensor,
         _dev(bitmap, torch.int32, p.words, "bitmap"),
         _dev(counters, torch.float32, p.c, "counters"),
         _dev(nnz_out, torch.int64, 1, "nnz_out"), _stream(stream)))
+
+
+def _ptrs(ts, dtype, numel, name):
+    return (ctypes.c_void_p * len(ts))(*[_dev(t, dtype, numel, name) for t in ts])
+
+
+def sketch_compress_batch(p: lhc_params, xs, bitmaps, counters, ds=None,
+                          nnz_out: torch.Tensor | None = None, stream=None):
+    """xs[b] (len ds[b] <= p.d, default p.d) into (bitmaps[b], counters[b]), one launch."""
+    n = len(xs)
+    if not (n == len(bitmaps) == len(counters)) or n < 1:
+        raise ValueError("need as many inputs as sketches")
+    ds = [int(p.d)] * n if ds is None else [int(v) for v in ds]
+    xp = (ctypes.c_void_p * n)(*[_dev(x, torch.float32, dd, "xs[]") for x, dd in zip(xs, ds)])
+    dp = (ctypes.c_uint32 * n)(*ds)
+    bp = _ptrs(bitmaps, torch.int32, None, "bitmaps[]")  # kept alive across the call
+    yp = _ptrs(counters, torch.float32, p.c, "counters[]")
+    _check("sketch_compress_batch", lib().sketch_compress_batch(
+        ctypes.byref(p), n, ctypes.addressof(xp), ctypes.addressof(dp), ctypes.addressof(bp),
+        ctypes.addressof(yp), _dev(nnz_out, torch.int64, 1, "nnz_out"), _stream(stream)))
+
+
+def sketch_clear_batch(p: lhc_params, bitmaps, counters, stream=None):
+    n = len(bitmaps)
+    if n != len(counters) or n < 1:
+        raise ValueError("need as many bitmaps as counter arrays")
+    bp = _ptrs(bitmaps, torch.int32, p.words, "bitmaps[]")
+    yp = _ptrs(counters, torch.float32, p.c, "counters[]")
+    _check("sketch_clear_batch", lib().sketch_clear_batch(
+        ctypes.byref(p), n, ctypes.addressof(bp), ctypes.addressof(yp), _stream(stream)))
 
 
 def sketch_compress_coo(p: lhc_params, idx: torch.Tensor, val: torch.Tensor,

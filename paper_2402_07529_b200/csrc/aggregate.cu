@@ -68,10 +68,17 @@ void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* co
 // Zero a sketch with L2 evict-last stores: the lines stay L2-resident for the
 // compress reductions that follow (a cold sketch costs one random DRAM sector
 // read per first touch).
-__global__ void __launch_bounds__(256) k_clear(uint4* __restrict__ a, uint64_t na, uint32_t* __restrict__ b,
+// clear up to kMaxBatch sketches: blockIdx.y = sketch
+struct ClearBatch {
+    uint4* counters[kMaxBatch];
+    uint32_t* bitmap[kMaxBatch];
+};
+__global__ void __launch_bounds__(256) k_clear(const __grid_constant__ ClearBatch C, uint64_t na,
                                                uint64_t nb) {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    uint4* a = C.counters[blockIdx.y];
+    uint32_t* b = C.bitmap[blockIdx.y];
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t u = tid; u < na; u += stride)
@@ -82,14 +89,22 @@ __global__ void __launch_bounds__(256) k_clear(uint4* __restrict__ a, uint64_t n
                      : "memory");
 }
 
-void launch_clear(uint32_t* bitmap, uint64_t n_words, float* counters, uint64_t c, cudaStream_t s) {
+void launch_clear(int n, uint32_t* const* bitmaps, uint64_t n_words, float* const* counters,
+                  uint64_t c, cudaStream_t s) {
     // counters: c is a multiple of 32 floats; bitmap words: 16-byte groups + tail
-    const uint64_t units = std::max<uint64_t>(c / 4, n_words / 4);
-    const uint32_t blocks =
-        (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((units + 255) / 256, (uint64_t)num_sms() * 8));
-    k_clear<<<blocks, 256, 0, s>>>(reinterpret_cast<uint4*>(counters), c / 4,
-                                   bitmap, n_words);
-    count_launch();
+    for (int b0 = 0; b0 < n; b0 += kMaxBatch) {
+        const int nb = std::min(kMaxBatch, n - b0);
+        ClearBatch C{};
+        for (int b = 0; b < nb; b++) {
+            C.counters[b] = reinterpret_cast<uint4*>(counters[b0 + b]);
+            C.bitmap[b] = bitmaps[b0 + b];
+        }
+        const uint64_t units = std::max<uint64_t>(c / 4, n_words / 4);
+        const uint32_t blocks = (uint32_t)std::max<uint64_t>(
+            1, std::min<uint64_t>((units + 255) / 256, (uint64_t)num_sms() * 8 / nb + 1));
+        k_clear<<<dim3(blocks, nb), 256, 0, s>>>(C, c / 4, n_words);
+        count_launch();
+    }
 }
 
 }  // namespace lhc

@@ -155,8 +155,40 @@ int sketch_clear(const lhc_params* p, uint32_t* bitmap, float* counters, void* s
     reset_launches();
     if (int rc = validate(p)) return rc;
     if (!bitmap || !counters) return set_error(LHC_EINVAL, "NULL sketch buffer");
-    launch_clear(bitmap, p->m / 32, counters, p->c, (cudaStream_t)stream);
+    launch_clear(1, &bitmap, p->m / 32, &counters, p->c, (cudaStream_t)stream);
     return check_launch("sketch_clear");
+}
+
+int sketch_clear_batch(const lhc_params* p, int n, uint32_t* const* bitmaps, float* const* counters,
+                       void* stream) {
+    reset_launches();
+    if (int rc = validate(p)) return rc;
+    if (n < 1 || !bitmaps || !counters) return set_error(LHC_EINVAL, "need n >= 1 sketches");
+    for (int b = 0; b < n; b++)
+        if (!bitmaps[b] || !counters[b] || !aligned16(counters[b]))
+            return set_error(LHC_EINVAL, "sketch %d is NULL or its counters not 16-byte aligned", b);
+    launch_clear(n, bitmaps, p->m / 32, counters, p->c, (cudaStream_t)stream);
+    return check_launch("sketch_clear_batch");
+}
+
+static void compress_batches(const KParams& P, int n, const float* const* xs, const uint32_t* ds,
+                             uint32_t* const* bitmaps, float* const* counters,
+                             unsigned long long* nnz_out, cudaStream_t s) {
+    for (int b0 = 0; b0 < n; b0 += kMaxBatch) {
+        CompressBatch B{};
+        B.n = (uint32_t)std::min(kMaxBatch, n - b0);
+        uint64_t start = 0;
+        for (uint32_t b = 0; b < B.n; b++) {
+            B.x[b] = xs[b0 + b];
+            B.bitmap[b] = bitmaps[b0 + b];
+            B.counters[b] = counters[b0 + b];
+            B.d[b] = ds ? ds[b0 + b] : P.d;
+            B.start[b] = start;
+            start += ((uint64_t)B.d[b] + kTile - 1) / kTile;
+        }
+        B.start[B.n] = start;
+        if (start) launch_compress_dense(P, B, nnz_out, s);
+    }
 }
 
 int sketch_compress(const lhc_params* p, const float* x, uint32_t* bitmap, float* counters,
@@ -166,8 +198,25 @@ int sketch_compress(const lhc_params* p, const float* x, uint32_t* bitmap, float
     if (!x || !bitmap || !counters) return set_error(LHC_EINVAL, "NULL buffer");
     if (!aligned16(x) || !aligned16(counters) || !aligned16(bitmap))
         return set_error(LHC_EINVAL, "x, bitmap and counters must be 16-byte aligned");
-    launch_compress_dense(kparams(p), x, bitmap, counters, nnz_out, (cudaStream_t)stream);
+    compress_batches(kparams(p), 1, &x, nullptr, &bitmap, &counters, nnz_out, (cudaStream_t)stream);
     return check_launch("sketch_compress");
+}
+
+int sketch_compress_batch(const lhc_params* p, int n, const float* const* xs, const uint32_t* ds,
+                          uint32_t* const* bitmaps, float* const* counters,
+                          unsigned long long* nnz_out, void* stream) {
+    reset_launches();
+    if (int rc = validate(p)) return rc;
+    if (n < 1 || !xs || !bitmaps || !counters) return set_error(LHC_EINVAL, "need n >= 1 inputs");
+    for (int b = 0; b < n; b++) {
+        if (!xs[b] || !bitmaps[b] || !counters[b])
+            return set_error(LHC_EINVAL, "input %d has a NULL buffer", b);
+        if (!aligned16(xs[b]) || !aligned16(bitmaps[b]) || !aligned16(counters[b]))
+            return set_error(LHC_EINVAL, "input %d: x, bitmap and counters must be 16-byte aligned", b);
+        if (ds && ds[b] > p->d) return set_error(LHC_EINVAL, "ds[%d] = %u > d", b, ds[b]);
+    }
+    compress_batches(kparams(p), n, xs, ds, bitmaps, counters, nnz_out, (cudaStream_t)stream);
+    return check_launch("sketch_compress_batch");
 }
 
 int sketch_compress_coo(const lhc_params* p, uint64_t nnz, const uint32_t* idx,

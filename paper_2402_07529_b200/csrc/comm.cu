@@ -292,25 +292,38 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
     const uint32_t epoch = *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot);
     const uint32_t par = *(volatile uint32_t*)(A.sig[A.rank] + kAgCountSlot) & 1u;
     const uint64_t n = min((uint64_t)*A.n_items, A.cap);
-    // push my list to every peer (value bits travel with the local index)
+    // A gather slot holds cap indices then cap values (cap a multiple of 4): the
+    // decoded list travels as two 16-byte-vector streams.
+    const uint64_t nv = n / 4;
+    const uint4* src_i = reinterpret_cast<const uint4*>(A.idx);
+    const uint4* src_v = reinterpret_cast<const uint4*>(A.val);
 #pragma unroll 1
     for (int dd = 1; dd < G; dd++) {
         const int q = (A.rank + dd) % G;
-        uint2* out = A.gather[q] + ((uint64_t)par * G + A.rank) * A.cap;
-        for (uint64_t i = gtid; i < n; i += gstride)
-            out[i] = make_uint2(__ldcg(A.idx + i), __float_as_uint(__ldcg(A.val + i)));
+        uint32_t* slot = reinterpret_cast<uint32_t*>(A.gather[q] + ((uint64_t)par * G + A.rank) * A.cap);
+        uint4* di = reinterpret_cast<uint4*>(slot);
+        uint4* dv = reinterpret_cast<uint4*>(slot + A.cap);
+        for (uint64_t u = gtid; u < nv; u += gstride) {
+            const uint4 a = __ldcg(src_i + u), b = __ldcg(src_v + u);
+            di[u] = a;
+            dv[u] = b;
+        }
+        for (uint64_t i = 4 * nv + gtid; i < n; i += gstride) {
+            slot[i] = __ldcg(A.idx + i);
+            slot[A.cap + i] = __float_as_uint(__ldcg(A.val + i));
+        }
         if (gtid == 0) A.sig[q][kGatherCountSlot + par * kMaxRanks + A.rank] = (uint32_t)n;
     }
-    // zero the peers' shard ranges of the local dense output meanwhile
+    // zero the peers' shard ranges [0, lo) and [hi, d) of the local dense output
+    // meanwhile (lo, hi multiples of 4 unless hi = d)
     {
         const uint64_t lo = (uint64_t)A.rank * A.shard_width;
         const uint64_t hi = min((uint64_t)A.d, lo + A.shard_width);
         float4* d4 = reinterpret_cast<float4*>(A.dense);
-        const uint64_t n4 = A.d / 4;  // shard_width is a multiple of 4
-        for (uint64_t u = gtid; u < n4; u += gstride)
-            if (4 * u < lo || 4 * u >= hi) __stcs(d4 + u, make_float4(0.f, 0.f, 0.f, 0.f));
-        for (uint64_t i = 4 * n4 + gtid; i < A.d; i += gstride)
-            if (i < lo || i >= hi) A.dense[i] = 0.f;
+        const uint64_t a4 = lo / 4, b4 = hi / 4, e4 = A.d / 4, own4 = b4 - a4;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint64_t u = gtid; u < e4 - own4; u += gstride) __stcs(d4 + (u < a4 ? u : u + own4), z);
+        for (uint64_t i = max(hi, 4 * e4) + gtid; i < A.d; i += gstride) A.dense[i] = 0.f;
     }
     sh_barrier<G>(grid, A, epoch + 1);
 #pragma unroll 1
@@ -319,11 +332,20 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
         const uint64_t nq = min((uint64_t)*(volatile uint32_t*)(A.sig[A.rank] + kGatherCountSlot +
                                                                par * kMaxRanks + q),
                                 A.cap);
-        const uint2* in = A.gather[A.rank] + ((uint64_t)par * G + q) * A.cap;
+        const uint32_t* slot = reinterpret_cast<const uint32_t*>(A.gather[A.rank] + ((uint64_t)par * G + q) * A.cap);
+        const uint4* si = reinterpret_cast<const uint4*>(slot);
+        const uint4* sv = reinterpret_cast<const uint4*>(slot + A.cap);
         float* base = A.dense + (uint64_t)q * A.shard_width;
-        for (uint64_t i = gtid; i < nq; i += gstride) {
-            const uint2 e = __ldcs(in + i);
-            if (e.y) base[e.x] = __uint_as_float(e.y);
+        for (uint64_t u = gtid; u < nq / 4; u += gstride) {
+            const uint4 a = __ldcs(si + u), b = __ldcs(sv + u);
+            if (b.x) base[a.x] = __uint_as_float(b.x);
+            if (b.y) base[a.y] = __uint_as_float(b.y);
+            if (b.z) base[a.z] = __uint_as_float(b.z);
+            if (b.w) base[a.w] = __uint_as_float(b.w);
+        }
+        for (uint64_t i = (nq & ~3ull) + gtid; i < nq; i += gstride) {
+            const uint32_t v = slot[A.cap + i];
+            if (v) base[slot[i]] = __uint_as_float(v);
         }
     }
     // every block read epoch / par before the barrier's grid syncs
@@ -371,6 +393,7 @@ static int shard_layout(const lhc_params* ps, int world, uint64_t cap, size_t* s
     if (int rc = validate(ps)) return rc;
     if (world < 1 || world > kMaxRanks) return set_error(LHC_EINVAL, "world must be in [1, 8]");
     if (cap == 0 || cap >= (1ull << 32)) return set_error(LHC_EINVAL, "cap_items must be in [1, 2^32)");
+    cap = (cap + 3) / 4 * 4;  // gather slots hold 16-byte vectors
     *y_off = align_up(ps->m / 8, 256);
     *slot = align_up(*y_off + ps->c * sizeof(float), 256);
     *stage = *slot * world;
@@ -577,7 +600,7 @@ int lhc_shard_comm_create(int rank, int world, const void* handles, const uint64
     c->sharded = 1;
     c->slot_bytes = slot;
     c->y_off = y;
-    c->cap = cap_items;
+    c->cap = (cap_items + 3) / 4 * 4;
     c->stage_off = st;
     c->gather_off = ga;
     c->signals_off = sg;
@@ -623,6 +646,8 @@ int sketch_allgather_decoded(lhc_comm* c, const uint32_t* idx, const float* val,
                              float* dense, void* stream) {
     if (!c || !c->sharded) return set_error(LHC_EINVAL, "not a sharded communicator");
     if (!idx || !val || !n_items || !dense) return set_error(LHC_EINVAL, "NULL argument");
+    if (((uintptr_t)idx | (uintptr_t)val | (uintptr_t)dense) & 15u)
+        return set_error(LHC_EINVAL, "idx, val and dense must be 16-byte aligned");
     if (shard_width == 0 || shard_width % 4 || (uint64_t)(c->world - 1) * shard_width >= d)
         return set_error(LHC_EINVAL, "shard_width must be a positive multiple of 4, every shard non-empty");
     reset_launches();

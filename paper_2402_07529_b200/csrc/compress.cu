@@ -112,9 +112,16 @@ __host__ __device__ constexpr size_t compress_warp_smem(uint32_t n_map) {
             ((n_map * 8 + 15) / 16) * 16 + kStages * sizeof(uint64_t) + 127) / 128 * 128;
 }
 
+// input of a global chunk index (the batch's chunk ranges are consecutive)
+__device__ __forceinline__ uint32_t batch_input(const CompressBatch& B, uint64_t g) {
+    uint32_t b = 0;
+    while (b + 1 < B.n && g >= B.start[b + 1]) b++;
+    return b;
+}
+
 __global__ void __launch_bounds__(kCompressThreads)
-k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ bitmap,
-                 float* __restrict__ counters, unsigned long long* __restrict__ nnz_out) {
+k_compress_dense(KParams P, const __grid_constant__ CompressBatch B,
+                 unsigned long long* __restrict__ nnz_out) {
     extern __shared__ __align__(128) unsigned char sh_all[];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t kk = P.k + P.kb;
@@ -125,8 +132,7 @@ k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ 
     uint2* sh_map = reinterpret_cast<uint2*>(sh_pos + kTile);
     uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sh_map) +
                                                 ((n_map * 8 + 15) / 16) * 16);
-    const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
-    const uint64_t nfull = (uint64_t)P.d / kTile;  // chunks that are whole (bulk-copied)
+    const uint64_t nchunks = B.start[B.n];  // chunks of all inputs
     const uint64_t stride = (uint64_t)gridDim.x * kCompressWarps;
     const uint64_t first = blockIdx.x * (uint64_t)kCompressWarps + warp;
     const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
@@ -139,25 +145,31 @@ k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ 
     }
     __syncwarp();
     // prologue: the first kStages - 1 chunks in flight
-    if (lane == 0) {
-        for (int st = 0; st < kStages - 1; st++) {
-            const uint64_t ch = first + st * stride;
-            if (ch < nfull) bulk_load(sh_x + st * kTile, x + ch * kTile, kTile * 4, bar + st, pol_stream);
-        }
-    }
-    uint32_t it = 0;
+    // whole chunks are bulk-copied; the ragged last chunk of an input is loaded plainly
+    auto prefetch = [&](uint64_t g, uint32_t sa) {
+        if (g >= nchunks) return;
+        const uint32_t b = batch_input(B, g);
+        const uint64_t lc = g - B.start[b];
+        if (lc < (uint64_t)B.d[b] / kTile)
+            bulk_load(sh_x + sa * kTile, B.x[b] + lc * kTile, kTile * 4, bar + sa, pol_stream);
+    };
+    if (lane == 0)
+        for (int st = 0; st < kStages - 1; st++) prefetch(first + st * stride, st);
+    uint32_t it = 0, phase = 0;
     for (uint64_t chunk = first; chunk < nchunks; chunk += stride, it++) {
         const uint32_t st = it % kStages;
         // refill: the stage consumed in the previous iteration takes chunk + (kStages-1) stride
-        {
-            const uint64_t ahead = chunk + (uint64_t)(kStages - 1) * stride;
-            if (lane == 0 && ahead < nfull) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                const uint32_t sa = (it + kStages - 1) % kStages;
-                bulk_load(sh_x + sa * kTile, x + ahead * kTile, kTile * 4, bar + sa, pol_stream);
-            }
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            prefetch(chunk + (uint64_t)(kStages - 1) * stride, (it + kStages - 1) % kStages);
         }
-        const uint64_t base = chunk * kTile;
+        const uint32_t bi = batch_input(B, chunk);
+        const uint64_t lchunk = chunk - B.start[bi];
+        const uint32_t d_in = B.d[bi];
+        const float* __restrict__ x = B.x[bi];
+        uint32_t* __restrict__ bitmap = B.bitmap[bi];
+        float* __restrict__ counters = B.counters[bi];
+        const uint64_t base = lchunk * kTile;
         float* cx = sh_x + st * kTile;
         // row maps of the chunk's rows (overlap the copy)
         const uint64_t row0 = base >> P.log2L;
@@ -166,10 +178,13 @@ k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ 
             const uint32_t dom = jj < P.k ? 0u : 1u;
             sh_map[a] = dom_map(P, dom, dom ? jj - P.k : jj, row0 + r);
         }
-        if (chunk < nfull) {
-            mbar_wait(bar + st, (it / kStages) & 1u);
+        if (lchunk < (uint64_t)d_in / kTile) {
+            // a stage's barrier completes one phase per bulk copy it received (ragged
+            // chunks of the batch's inputs receive none): track its parity explicitly
+            mbar_wait(bar + st, (phase >> st) & 1u);
+            phase ^= 1u << st;
         } else {  // ragged last chunk: plain loads
-            for (uint32_t a = lane; a < kTile; a += 32) cx[a] = base + a < P.d ? x[base + a] : 0.f;
+            for (uint32_t a = lane; a < kTile; a += 32) cx[a] = base + a < d_in ? x[base + a] : 0.f;
         }
         __syncwarp();
         // nonzero words: lane w builds word w from its 32 values (eight 16-byte
@@ -245,9 +260,9 @@ k_compress_dense(KParams P, const float* __restrict__ x, uint32_t* __restrict__ 
     }
 }
 
-void launch_compress_dense(const KParams& P, const float* x, uint32_t* bitmap, float* counters,
-                           unsigned long long* nnz_out, cudaStream_t s) {
-    const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
+void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned long long* nnz_out,
+                           cudaStream_t s) {
+    const uint64_t nchunks = B.start[B.n];
     const uint32_t n_map = (kTile >> P.log2L) * (P.k + P.kb);
     const size_t smem = kCompressWarps * compress_warp_smem(n_map);
     static int per_sm[64][6] = {};
@@ -263,7 +278,7 @@ void launch_compress_dense(const KParams& P, const float* x, uint32_t* bitmap, f
     }
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((nchunks + kCompressWarps - 1) / kCompressWarps,
                                                          (uint64_t)num_sms() * (dev < 64 ? per_sm[dev][key] : 2));
-    k_compress_dense<<<blocks, kCompressThreads, smem, s>>>(P, x, bitmap, counters, nnz_out);
+    k_compress_dense<<<blocks, kCompressThreads, smem, s>>>(P, B, nnz_out);
     count_launch();
 }
 

@@ -16,11 +16,24 @@ int validate(const lhc_params* p);
 KParams kparams(const lhc_params* p);
 
 void launch_hash_rows(const KParams& P, uint32_t dom, uint64_t n_rows, uint2* out, cudaStream_t s);
-void launch_compress_dense(const KParams& P, const float* x, uint32_t* bitmap, float* counters,
-                           unsigned long long* nnz_out, cudaStream_t s);
+// up to kMaxBatch dense inputs compressed by one launch: input b (d[b] <= P.d
+// coordinates) into (bitmap[b], counters[b]); its chunks are the global chunk
+// indices [start[b], start[b + 1])
+constexpr int kMaxBatch = 16;
+struct CompressBatch {
+    const float* x[kMaxBatch];
+    uint32_t* bitmap[kMaxBatch];
+    float* counters[kMaxBatch];
+    uint64_t start[kMaxBatch + 1];
+    uint32_t d[kMaxBatch];
+    uint32_t n;
+};
+void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned long long* nnz_out,
+                           cudaStream_t s);
 void launch_compress_coo(const KParams& P, uint64_t nnz, const uint32_t* idx, const float* val,
                          uint32_t* bitmap, float* counters, cudaStream_t s);
-void launch_clear(uint32_t* bitmap, uint64_t n_words, float* counters, uint64_t c, cudaStream_t s);
+void launch_clear(int n, uint32_t* const* bitmaps, uint64_t n_words, float* const* counters,
+                  uint64_t c, cudaStream_t s);
 void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* const* bitmaps,
                       const float* const* counters, uint32_t* out_bitmap, float* out_counters,
                       cudaStream_t s);

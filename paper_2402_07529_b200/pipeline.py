@@ -161,21 +161,21 @@ class LosslessAllReduce:
         return self._step(list(coos), stream)
 
     def _step(self, items, stream):
-        def compress(sk, item):
-            if len(item) == 1:
-                sk.compress(item[0], stream=stream)
-            else:
-                sk.compress_coo(item[0], item[1], stream=stream)
-
+        targets = self.worker_sketches if self.per_worker else [self.sketch]
+        L.sketch_clear_batch(self.p, [t.bitmap for t in targets], [t.counters for t in targets],
+                             stream)
         if self.per_worker:
-            for sk, item in zip(self.worker_sketches, items):
-                sk.clear(stream)
-                compress(sk, item)
-            aggregate(self.p, self.worker_sketches, self.sketch, stream)
+            dst = self.worker_sketches[:len(items)]
         else:
-            self.sketch.clear(stream)
-            for item in items:
-                compress(self.sketch, item)
+            dst = [self.sketch] * len(items)
+        if all(len(it) == 1 for it in items):   # dense: one launch for all workers
+            L.sketch_compress_batch(self.p, [it[0] for it in items], [t.bitmap for t in dst],
+                                    [t.counters for t in dst], stream=stream)
+        else:
+            for sk, it in zip(dst, items):
+                sk.compress_coo(it[0], it[1], stream=stream)
+        if self.per_worker:
+            aggregate(self.p, self.worker_sketches, self.sketch, stream)
         if self.comm is not None and self.comm.world > 1:
             self.comm.allreduce(stream)
         return self.decoder(self.sketch, stream)
@@ -184,9 +184,10 @@ class LosslessAllReduce:
 class _SlotSketch:
     """A Sketch-like view of slot q of a sharded buffer (bitmap and counters of one shard)."""
 
-    def __init__(self, p: L.lhc_params, buf: torch.Tensor, base: int, y_off: int):
+    def __init__(self, p: L.lhc_params, buf: torch.Tensor, base: int, y_off: int, words: int):
         self.p = p
-        self.bitmap = buf[base:base + p.words * 4].view(torch.int32)
+        # the view spans the slot's whole bitmap region (the largest shard's words)
+        self.bitmap = buf[base:base + words * 4].view(torch.int32)
         self.counters = buf[base + y_off:base + y_off + int(p.c) * 4].view(torch.float32)
 
     clear = Sketch.clear
@@ -223,7 +224,8 @@ class ShardedAllReduce:
         self.cap = min(self.cap, plan.width)
         self.slot_bytes, self.y_off, total = L.lhc_shard_layout(self.ps[0], self.world, self.cap)
         self.buf = torch.zeros(total, dtype=torch.uint8, device=device)
-        self.slots = [_SlotSketch(self.ps[q], self.buf, q * self.slot_bytes, self.y_off)
+        words = self.ps[0].words
+        self.slots = [_SlotSketch(self.ps[q], self.buf, q * self.slot_bytes, self.y_off, words)
                       for q in range(plan.shards)]
         self.per_worker = per_worker and local_workers > 1
         self.worker_bufs = []
@@ -231,7 +233,7 @@ class ShardedAllReduce:
             for _ in range(local_workers):
                 b = torch.zeros(self.slot_bytes * plan.shards, dtype=torch.uint8, device=device)
                 self.worker_bufs.append(
-                    [_SlotSketch(self.ps[q], b, q * self.slot_bytes, self.y_off)
+                    [_SlotSketch(self.ps[q], b, q * self.slot_bytes, self.y_off, words)
                      for q in range(plan.shards)])
         self.dense = torch.empty(plan.d, dtype=torch.float32, device=device)
         # the shards this process decodes: its own, or all of them on one rank
@@ -278,29 +280,31 @@ class ShardedAllReduce:
             out.append(((idx[a:b] - lo).astype(idx.dtype), val[a:b]))
         return out
 
-    def _compress_all(self, slots, item, stream, coo=False):
-        for q, sk in enumerate(slots):
-            if coo:
-                sk.compress_coo(item[q][0], item[q][1], stream=stream)
-            else:
-                sk.compress(self.shard_input(item[0], q), stream=stream)
-
     def _step(self, items, stream, coo=False):
         G = self.plan.shards
+        targets = self.worker_bufs[:len(items)] if self.per_worker else [self.slots] * len(items)
+        clear = self.worker_bufs if self.per_worker else [self.slots]
+        flat = [sk for bufs in clear for sk in bufs]
+        L.sketch_clear_batch(self.ps[0], [sk.bitmap for sk in flat], [sk.counters for sk in flat],
+                             stream)
+        if coo:
+            for bufs, item in zip(targets, items):
+                for q, sk in enumerate(bufs):
+                    sk.compress_coo(item[q][0], item[q][1], stream=stream)
+        else:   # every (worker, shard) pair in one launch
+            xs, bms, ys, ds = [], [], [], []
+            for bufs, item in zip(targets, items):
+                for q, sk in enumerate(bufs):
+                    xs.append(self.shard_input(item[0], q))
+                    bms.append(sk.bitmap)
+                    ys.append(sk.counters)
+                    ds.append(self.plan.shard_d(q))
+            L.sketch_compress_batch(self.ps[0], xs, bms, ys, ds=ds, stream=stream)
         if self.per_worker:
-            for bufs, item in zip(self.worker_bufs, items):
-                for sk in bufs:
-                    sk.clear(stream)
-                self._compress_all(bufs, item, stream, coo)
             for q in range(G):
                 L.sketch_aggregate(self.ps[q], [b[q].bitmap for b in self.worker_bufs],
                                    [b[q].counters for b in self.worker_bufs],
                                    self.slots[q].bitmap, self.slots[q].counters, stream)
-        else:
-            for sk in self.slots:
-                sk.clear(stream)
-            for item in items:
-                self._compress_all(self.slots, item, stream, coo)
         if self.world > 1:
             L.sketch_reduce_scatter(self.handle, stream)
         for q in self.owned:

@@ -415,8 +415,36 @@ def test_sharded_single_process(lhc, ora, d, nnz, W, G, kb, law):
         lo, hi = plan.bounds(q)
         p = run.ps[q]
         B, Y, ref = ora.pipeline(ora_params(ora, p), [x[lo:hi] for x in xs])
-        assert np.array_equal(U(run.slots[q].bitmap), B)
+        bm = U(run.slots[q].bitmap)
+        assert np.array_equal(bm[:p.words], B) and not bm[p.words:].any()
         assert_values(F(run.slots[q].counters), Y, law == "dyadic")
         compare_decode(ora, run.decoders[q], ref, law == "dyadic")
         assert_values(dense[lo:hi], ref.dense, law == "dyadic")
     assert dec is run.decoders[0]
+
+
+def test_compress_batch_chained_and_repeated(lhc, ora):
+    """sketch_compress_batch over more than 16 inputs (two launches) with repeated
+    target sketches and ragged input lengths equals the oracle's per-input
+    compression accumulated per target (homomorphism)."""
+    d, W = 50_000, 18
+    s = lhc.size_workload(d, 0.02, W)
+    p = gpu_params(lhc, d, s.m, s.c, seed=0xBA7C)
+    xs = make_workers(d, 1000, W, 5, "dyadic")
+    ds = [d - 97 * (w % 3) for w in range(W)]          # some inputs shorter than d
+    sks = [lhc.Sketch(p) for _ in range(3)]
+    lhc.sketch_clear_batch(p, [k.bitmap for k in sks], [k.counters for k in sks])
+    tgt = [sks[w % 3] for w in range(W)]
+    lhc.sketch_compress_batch(p, [torch.from_numpy(x).cuda() for x in xs],
+                              [t.bitmap for t in tgt], [t.counters for t in tgt], ds=ds)
+    torch.cuda.synchronize()
+    op = ora_params(ora, p)
+    for r in range(3):
+        parts = []
+        for w in range(r, W, 3):
+            x = xs[w].copy()
+            x[ds[w]:] = 0.0                                  # coordinates past ds[w] are not read
+            parts.append(ora.compress_dense(op, x))
+        B, Y = ora.aggregate([a for a, _ in parts], [b for _, b in parts])
+        assert np.array_equal(U(sks[r].bitmap), B)
+        assert np.array_equal(F(sks[r].counters), Y)

@@ -52,7 +52,9 @@ def parse():
                     help="Bloom filter (default), exact bitmap (P:L188), or the smaller of the two")
     ap.add_argument("--fuse-local", action="store_true",
                     help="compress a rank's workers straight into one sketch (no per-worker sketches)")
-    ap.add_argument("--comm", choices=["p2p", "nccl"], default="p2p")
+    ap.add_argument("--comm", choices=["p2p", "nvls", "nccl"], default="p2p",
+                    help="p2p: NVLink peer stores (two-shot); nvls: NVSwitch multicast "
+                         "(in-switch reduction, NEXT-2); nccl: the NCCL baseline")
     ap.add_argument("--decode", choices=["replicated", "sharded"], default="replicated",
                     help="replicated: all-reduce, every rank decodes all of d (the north "
                          "star); sharded: per-shard sub-sketches, reduce-scatter, every rank "
@@ -247,16 +249,18 @@ def main():
     if sharded:
         from paper_2402_07529_b200.sizing import shard_plan
 
-        if args.comm != "p2p":
-            raise SystemExit("--decode sharded uses the NVLink P2P reduce-scatter")
+        if args.comm == "nccl":
+            raise SystemExit("--decode sharded needs --comm p2p or nvls")
         plan = shard_plan(wl.d, world, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb)
         run = lhc.ShardedAllReduce(plan, seed=SEED, local_workers=len(xs),
-                                   per_worker=not args.fuse_local, device=dev)
+                                   per_worker=not args.fuse_local, device=dev, comm=args.comm)
         p_dec = run.ps[rank]           # the shard this rank decodes
         G = plan.shards
     else:
         if world > 1 and args.comm == "p2p":
             comm = lhc.PeerComm(p)
+        elif world > 1 and args.comm == "nvls":
+            comm = lhc.NvlsComm(p)
         run = lhc.LosslessAllReduce(p, cap, local_workers=len(xs),
                                     per_worker=not args.fuse_local, comm=comm, device=dev)
         p_dec = p
@@ -343,7 +347,7 @@ def main():
                 cnt()
         mark("aggregate")
         if world > 1:
-            lhc.sketch_reduce_scatter(run.handle)
+            run.reduce_scatter()
             cnt()
         mark("allreduce")
         dec = run.decoder
@@ -354,8 +358,7 @@ def main():
         cnt()
         mark("peel")
         if world > 1:
-            lhc.sketch_allgather_decoded(run.handle, dec.idx, dec.val, dec.stats, run.plan.width,
-                                         wl.d, run.dense)
+            run.allgather()
             cnt()
         mark("allgather")
 
@@ -577,7 +580,8 @@ def main():
             "k_peel": (16 * int(p_dec.c) + 9 * n_c + 4 * int(p_dec.d), 1, per_step_ms["peel"],
                        hbm, "hbm"),
             # the own list to every peer (8 B per item)
-            "k_allgather_decoded": (8 * n_c * (world - 1), 1 if world > 1 else 0,
+            "k_allgather_decoded": (8 * n_c * (1 if args.comm == "nvls" else world - 1),
+                                    1 if world > 1 else 0,
                                     per_step_ms["allgather"], nvl, "nvlink"),
         }
     else:
@@ -586,7 +590,10 @@ def main():
             "k_compress_dense": (W_loc * (4 * wl.d + S), 1, avg_compress_ms, hbm, "hbm"),
             "k_aggregate": ((W_loc + 1) * S, 1 if run.per_worker else 0,
                             per_step_ms["aggregate"], hbm, "hbm"),
-            "k_allreduce": (2 * (world - 1) / world * S, 1 if world > 1 else 0,
+            # NVLink bytes out per rank: two-shot 2(G-1)/G S; NVLS (the switch pulls
+            # every operand, one multicast store per slice) (1 + 1/G) S
+            "k_allreduce": ((1 + 1 / world) * S if args.comm == "nvls" else 2 * (world - 1) / world * S,
+                            1 if world > 1 and args.comm != "nccl" else 0,
                             per_step_ms["allreduce"], nvl, "nvlink"),
             "k_query": (int(p.m) // 8 + 4 * n_c, 1, per_step_ms["query"], hbm, "hbm"),
             # peel + finalize, and the dense output (zeroed, then the values at candidates)
@@ -628,8 +635,7 @@ def main():
                        "sketch_bytes": int(p.m) // 8 + 4 * int(p.c),
                        "per_worker_sketches": run.per_worker,
                        "decode": args.decode,
-                       "comm": ("p2p" if comm is not None or sharded else "nccl")
-                       if world > 1 else "none",
+                       "comm": args.comm if world > 1 else "none",
                        "l2": "flushed (256 MB write) between timed steps, outside the events",
                        "cuda_graph": graph is not None,
                        "kernel_timing": "CUDA events between kernels in a second K-step pass "

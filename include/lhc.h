@@ -207,6 +207,42 @@ int sketch_allgather_decoded(lhc_comm* comm, const uint32_t* idx, const float* v
                              const unsigned long long* n_items /*device*/, uint64_t shard_width,
                              uint32_t d, float* dense, void* stream);
 
+/* In-switch aggregation over an NVSwitch multicast object (NVLS; DESIGN.md
+ * NEXT-2 — the paper's in-network aggregation, P:L122-124 / P:L283, done by the
+ * switch).  Collective setup, every rank of the same `world`:
+ *   lhc_nvls_open  rank 0 creates a multicast object of >= bytes (+ a 4 KB signal
+ *                  area) and hands it to the other ranks over the abstract Unix
+ *                  socket `rendezvous` (a name unique to this group); every rank
+ *                  adds its current device.  LHC_ECOMM if the box has no NVLS.
+ *   (all ranks must return from lhc_nvls_open before any calls lhc_nvls_bind,
+ *    e.g. a process-group barrier in between)
+ *   lhc_nvls_bind  binds a zeroed buffer of this device to the object and returns
+ *                  its local pointer and usable size: lay the sketch out in it
+ *                  exactly as for lhc_comm_layout (replicated) or
+ *                  lhc_shard_layout (sharded) and compress straight into it.
+ * Then, with the same call sequence on every rank:
+ *   sketch_allreduce_nvls        [bitmap | counters] (lhc_comm_layout offsets) becomes
+ *        the OR / sum over ranks on every rank: each rank reduces a 1/world slice
+ *        with multimem.ld_reduce (the switch reads every rank's copy) and writes
+ *        it to every rank with one multimem.st; two switch-counter barriers.
+ *   sketch_reduce_scatter_nvls   sharded layout: slot `rank` becomes the OR / sum
+ *        over ranks of their slot `rank` (multimem.ld_reduce, local store).
+ *   sketch_allgather_decoded_nvls  as sketch_allgather_decoded, the list written
+ *        once with multicast stores (the switch replicates it to every rank).
+ * The in-switch fp32 sum is identical on every rank (one rank reduces each
+ * element and broadcasts it) but its order is the switch's, not ascending rank.
+ * lhc_nvls_destroy unmaps and releases (after the last call completed). */
+typedef struct lhc_nvls lhc_nvls;
+int lhc_nvls_open(int rank, int world, const char* rendezvous, size_t bytes, lhc_nvls** out);
+int lhc_nvls_bind(lhc_nvls* h, void** local_ptr, size_t* size);
+int sketch_allreduce_nvls(lhc_nvls* h, const lhc_params* p, void* stream);
+int sketch_reduce_scatter_nvls(lhc_nvls* h, const lhc_params* ps, uint64_t cap_items, void* stream);
+int sketch_allgather_decoded_nvls(lhc_nvls* h, const lhc_params* ps, uint64_t cap_items,
+                                  const uint32_t* idx, const float* val,
+                                  const unsigned long long* n_items /*device*/,
+                                  uint64_t shard_width, uint32_t d, float* dense, void* stream);
+void lhc_nvls_destroy(lhc_nvls* h);
+
 /* ---- Phase II: recovery (Alg. 1) ----------------------------- */
 
 /* Decode an aggregated sketch [bitmap, counters] (not modified):

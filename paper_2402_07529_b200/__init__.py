@@ -36,6 +36,8 @@ from ._lib import (  # noqa: F401
 from .pipeline import (  # noqa: F401
     Decoder,
     LosslessAllReduce,
+    NvlsBuffer,
+    NvlsComm,
     PeerComm,
     ShardedAllReduce,
     Sketch,

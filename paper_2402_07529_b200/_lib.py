@@ -80,7 +80,8 @@ EXPORTS = [
     "sketch_allreduce", "lhc_comm_destroy", "sketch_decompress", "lhc_last_launch_count",
     "sketch_query", "sketch_peel", "lhc_shard_layout", "lhc_shard_comm_create",
     "sketch_reduce_scatter", "sketch_allgather_decoded", "sketch_compress_batch",
-    "sketch_clear_batch",
+    "sketch_clear_batch", "lhc_nvls_open", "lhc_nvls_bind", "sketch_allreduce_nvls",
+    "sketch_reduce_scatter_nvls", "sketch_allgather_decoded_nvls", "lhc_nvls_destroy",
 ]
 
 
@@ -122,6 +123,12 @@ def lib() -> ctypes.CDLL:
             "sketch_allgather_decoded": (i32, [vp, vp, vp, vp, u64, u32, vp, vp]),
             "sketch_compress_batch": (i32, [P, i32, vp, vp, vp, vp, vp, vp]),
             "sketch_clear_batch": (i32, [P, i32, vp, vp, vp]),
+            "lhc_nvls_open": (i32, [i32, i32, ctypes.c_char_p, sz, ctypes.POINTER(vp)]),
+            "lhc_nvls_bind": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(sz)]),
+            "sketch_allreduce_nvls": (i32, [vp, P, vp]),
+            "sketch_reduce_scatter_nvls": (i32, [vp, P, u64, vp]),
+            "sketch_allgather_decoded_nvls": (i32, [vp, P, u64, vp, vp, vp, u64, u32, vp, vp]),
+            "lhc_nvls_destroy": (None, [vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -348,6 +355,53 @@ def sketch_allgather_decoded(comm: int, idx: torch.Tensor, val: torch.Tensor, st
         comm, _dev(idx, torch.int32, None, "idx"), _dev(val, torch.float32, None, "val"),
         _dev(stats, torch.uint8, STATS_BYTES, "stats"), int(shard_width), int(d),
         _dev(dense, torch.float32, d, "dense"), _stream(stream)))
+
+
+def lhc_nvls_open(rank: int, world: int, rendezvous: str, nbytes: int) -> int:
+    out = ctypes.c_void_p()
+    _check("lhc_nvls_open", lib().lhc_nvls_open(rank, world, rendezvous.encode(), int(nbytes),
+                                                ctypes.byref(out)))
+    return out.value
+
+
+def lhc_nvls_bind(h: int) -> tuple[int, int]:
+    ptr, size = ctypes.c_void_p(), ctypes.c_size_t()
+    _check("lhc_nvls_bind", lib().lhc_nvls_bind(h, ctypes.byref(ptr), ctypes.byref(size)))
+    return int(ptr.value), int(size.value)
+
+
+def sketch_allreduce_nvls(h: int, p: lhc_params, stream=None):
+    _check("sketch_allreduce_nvls", lib().sketch_allreduce_nvls(h, ctypes.byref(p), _stream(stream)))
+
+
+def sketch_reduce_scatter_nvls(h: int, ps: lhc_params, cap_items: int, stream=None):
+    _check("sketch_reduce_scatter_nvls",
+           lib().sketch_reduce_scatter_nvls(h, ctypes.byref(ps), int(cap_items), _stream(stream)))
+
+
+def sketch_allgather_decoded_nvls(h: int, ps: lhc_params, cap_items: int, idx, val, stats,
+                                  shard_width: int, d: int, dense, stream=None):
+    _check("sketch_allgather_decoded_nvls", lib().sketch_allgather_decoded_nvls(
+        h, ctypes.byref(ps), int(cap_items), _dev(idx, torch.int32, None, "idx"),
+        _dev(val, torch.float32, None, "val"), _dev(stats, torch.uint8, STATS_BYTES, "stats"),
+        int(shard_width), int(d), _dev(dense, torch.float32, d, "dense"), _stream(stream)))
+
+
+def lhc_nvls_destroy(h: int):
+    lib().lhc_nvls_destroy(h)
+
+
+class _DevPtr:
+    """__cuda_array_interface__ view of a device allocation owned by liblhc.so."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def device_bytes(ptr: int, nbytes: int, device) -> torch.Tensor:
+    """A uint8 tensor over nbytes at ptr (no copy; the caller keeps the owner alive)."""
+    return torch.as_tensor(_DevPtr(ptr, nbytes), device=device)
 
 
 def lhc_comm_destroy(comm: int):

@@ -675,3 +675,504 @@ void lhc_comm_destroy(lhc_comm* c) {
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// NVLS: in-switch aggregation through an NVSwitch multicast object (DESIGN.md
+// NEXT-2; the paper's in-network aggregation, P:L122-124 / P:L283, done by the
+// switch).  Every rank binds its own physical buffer to one multicast object and
+// maps it twice: unicast (local loads/stores, where the sketch is compressed) and
+// multicast (multimem.* instructions, which the switch applies to every rank's
+// copy):
+//   multimem.ld_reduce .add.f32 / .or.b64   the switch reads the address on every
+//                                           rank and returns the sum / OR
+//   multimem.st                              one store reaches every rank's copy
+//   multimem.red.add.u32                     barrier counter on every rank
+// The multicast handle travels as a POSIX file descriptor over an abstract Unix
+// socket (SCM_RIGHTS) from rank 0 to the others.
+// ===========================================================================
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <unistd.h>
+
+#include <chrono>
+#include <thread>
+
+namespace lhc {
+
+constexpr size_t kNvlsSig = 4096;  // signal area at the end of the mapping
+constexpr int kNvU = 4;            // multimem reductions in flight per thread
+
+__device__ __forceinline__ void mm_or_b64(uint64_t* mc, uint64_t* out) {
+    asm volatile("multimem.ld_reduce.weak.global.or.b64 %0, [%1];" : "=l"(*out) : "l"(mc) : "memory");
+}
+__device__ __forceinline__ float4 mm_add_v4f32(const float* mc) {
+    float4 v;
+    asm volatile("multimem.ld_reduce.weak.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(mc) : "memory");
+    return v;
+}
+__device__ __forceinline__ void mm_st_v4(float* mc, float4 v) {
+    asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};"
+                 ::"l"(mc), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ void mm_st_u32(uint32_t* mc, uint32_t v) {
+    asm volatile("multimem.st.weak.global.b32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+}
+
+struct NvArgs {
+    char* uc;              // local (unicast) view of the buffer
+    char* mc;              // multicast view
+    uint32_t* sig_uc;      // [0] barrier counter (multicast-updated), [16] epoch (local)
+    uint32_t* sig_mc;
+    int rank, world;
+    // regions in 16-byte units
+    uint64_t lo, hi, y_unit;      // all-reduce: units [0, hi) (bitmap below y_unit); slice by rank
+    uint64_t slot_units, cap;     // sharded layout
+    uint64_t gather_off;
+    const uint32_t* idx;
+    const float* val;
+    const unsigned long long* n_items;
+    float* dense;
+    uint64_t shard_width;
+    uint32_t d;
+};
+
+// all ranks: every thread's writes are ordered before the switch-wide counter
+// increment; block 0 waits for all ranks' increments
+__device__ void nv_barrier(cg::grid_group& grid, const NvArgs& A, uint32_t target) {
+    __threadfence_system();
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(A.sig_mc), "r"(1u) : "memory");
+        while ((int32_t)(ld_acquire_sys(A.sig_uc) - target) < 0) {
+        }
+        asm volatile("fence.proxy.alias;" ::: "memory");
+    }
+    grid.sync();
+}
+
+// 16-byte unit u of the multicast view: OR (bitmap) or sum (counters) over ranks
+__device__ __forceinline__ float4 nv_reduce_unit(const NvArgs& A, uint64_t off_bytes, bool is_or) {
+    if (is_or) {
+        uint64_t a, b;
+        mm_or_b64(reinterpret_cast<uint64_t*>(A.mc + off_bytes), &a);
+        mm_or_b64(reinterpret_cast<uint64_t*>(A.mc + off_bytes + 8), &b);
+        float4 v;
+        v.x = __uint_as_float((uint32_t)a);
+        v.y = __uint_as_float((uint32_t)(a >> 32));
+        v.z = __uint_as_float((uint32_t)b);
+        v.w = __uint_as_float((uint32_t)(b >> 32));
+        return v;
+    }
+    return mm_add_v4f32(reinterpret_cast<const float*>(A.mc + off_bytes));
+}
+
+__global__ void __launch_bounds__(256) k_allreduce_nvls(NvArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t epoch = *(volatile uint32_t*)(A.sig_uc + 16);
+    nv_barrier(grid, A, (epoch + 1) * (uint32_t)A.world);  // every rank's sketch is complete
+    // kNvU switch reductions in flight per thread
+    for (uint64_t u0 = A.lo + gtid; u0 < A.hi; u0 += kNvU * gstride) {
+        float4 v[kNvU];
+#pragma unroll
+        for (int a = 0; a < kNvU; a++) {
+            const uint64_t u = u0 + a * gstride;
+            if (u < A.hi) v[a] = nv_reduce_unit(A, u * 16, u < A.y_unit);
+        }
+#pragma unroll
+        for (int a = 0; a < kNvU; a++) {
+            const uint64_t u = u0 + a * gstride;
+            if (u < A.hi) mm_st_v4(reinterpret_cast<float*>(A.mc + u * 16), v[a]);
+        }
+    }
+    nv_barrier(grid, A, (epoch + 2) * (uint32_t)A.world);  // every slice is everywhere
+    if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile uint32_t*)(A.sig_uc + 16) = epoch + 2;
+}
+
+// sharded layout: slot `rank` (locally) = OR / sum over ranks of their slot `rank`
+__global__ void __launch_bounds__(256) k_reduce_scatter_nvls(NvArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t epoch = *(volatile uint32_t*)(A.sig_uc + 16);
+    nv_barrier(grid, A, (epoch + 1) * (uint32_t)A.world);
+    const uint64_t base = (uint64_t)A.rank * A.slot_units;
+    uint4* out = reinterpret_cast<uint4*>(A.uc) + base;
+    for (uint64_t u0 = gtid; u0 < A.slot_units; u0 += kNvU * gstride) {
+        float4 v[kNvU];
+#pragma unroll
+        for (int a = 0; a < kNvU; a++) {
+            const uint64_t u = u0 + a * gstride;
+            if (u < A.slot_units) v[a] = nv_reduce_unit(A, (base + u) * 16, u < A.y_unit);
+        }
+#pragma unroll
+        for (int a = 0; a < kNvU; a++) {
+            const uint64_t u = u0 + a * gstride;
+            if (u < A.slot_units) out[u] = *reinterpret_cast<const uint4*>(&v[a]);
+        }
+    }
+    // the peers may rewrite their slots (next step) only after every rank read them
+    nv_barrier(grid, A, (epoch + 2) * (uint32_t)A.world);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile uint32_t*)(A.sig_uc + 16) = epoch + 2;
+}
+
+// sharded layout: my decoded list -> gather slot [par][rank] of every rank with one
+// multicast store per 16 bytes; zero the peer ranges of dense; barrier; scatter
+__global__ void __launch_bounds__(256) k_allgather_nvls(NvArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t epoch = *(volatile uint32_t*)(A.sig_uc + 16);
+    const uint32_t par = *(volatile uint32_t*)(A.sig_uc + 17) & 1u;
+    const int G = A.world;
+    const uint64_t n = min((uint64_t)*A.n_items, A.cap);
+    const uint64_t slot_bytes = A.cap * 8;
+    {
+        const uint64_t off = A.gather_off + ((uint64_t)par * G + A.rank) * slot_bytes;
+        float* di = reinterpret_cast<float*>(A.mc + off);
+        float* dv = reinterpret_cast<float*>(A.mc + off + A.cap * 4);
+        const uint64_t nv = (n + 3) / 4;  // the source lists hold >= n rounded up to 4? no: guard
+        for (uint64_t u = gtid; u < nv; u += gstride) {
+            float4 a, b;
+            const uint64_t i0 = 4 * u;
+            a.x = __uint_as_float(i0 + 0 < n ? __ldcg(A.idx + i0 + 0) : 0u);
+            a.y = __uint_as_float(i0 + 1 < n ? __ldcg(A.idx + i0 + 1) : 0u);
+            a.z = __uint_as_float(i0 + 2 < n ? __ldcg(A.idx + i0 + 2) : 0u);
+            a.w = __uint_as_float(i0 + 3 < n ? __ldcg(A.idx + i0 + 3) : 0u);
+            b.x = i0 + 0 < n ? __ldcg(A.val + i0 + 0) : 0.f;
+            b.y = i0 + 1 < n ? __ldcg(A.val + i0 + 1) : 0.f;
+            b.z = i0 + 2 < n ? __ldcg(A.val + i0 + 2) : 0.f;
+            b.w = i0 + 3 < n ? __ldcg(A.val + i0 + 3) : 0.f;
+            mm_st_v4(di + i0, a);
+            mm_st_v4(dv + i0, b);
+        }
+        if (gtid == 0)
+            mm_st_u32(reinterpret_cast<uint32_t*>(A.sig_mc) + 64 + par * kMaxRanks + A.rank, (uint32_t)n);
+    }
+    {
+        const uint64_t lo = (uint64_t)A.rank * A.shard_width;
+        const uint64_t hi = min((uint64_t)A.d, lo + A.shard_width);
+        float4* d4 = reinterpret_cast<float4*>(A.dense);
+        const uint64_t a4 = lo / 4, b4 = hi / 4, e4 = A.d / 4, own4 = b4 - a4;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint64_t u = gtid; u < e4 - own4; u += gstride) __stcs(d4 + (u < a4 ? u : u + own4), z);
+        for (uint64_t i = max(hi, 4 * e4) + gtid; i < A.d; i += gstride) A.dense[i] = 0.f;
+    }
+    nv_barrier(grid, A, (epoch + 1) * (uint32_t)A.world);
+    for (int dd = 1; dd < G; dd++) {
+        const int q = (A.rank + dd) % G;
+        const uint64_t nq = min((uint64_t)*(volatile uint32_t*)(A.sig_uc + 64 + par * kMaxRanks + q), A.cap);
+        const char* slot = A.uc + A.gather_off + ((uint64_t)par * G + q) * slot_bytes;
+        const uint4* si = reinterpret_cast<const uint4*>(slot);
+        const uint4* sv = reinterpret_cast<const uint4*>(slot + A.cap * 4);
+        float* base = A.dense + (uint64_t)q * A.shard_width;
+        for (uint64_t u = gtid; u < (nq + 3) / 4; u += gstride) {
+            const uint4 a = __ldcs(si + u), b = __ldcs(sv + u);
+            if (b.x) base[a.x] = __uint_as_float(b.x);
+            if (b.y) base[a.y] = __uint_as_float(b.y);
+            if (b.z) base[a.z] = __uint_as_float(b.z);
+            if (b.w) base[a.w] = __uint_as_float(b.w);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *(volatile uint32_t*)(A.sig_uc + 16) = epoch + 1;
+        *(volatile uint32_t*)(A.sig_uc + 17) = par + 1;
+    }
+}
+
+}  // namespace lhc
+
+struct lhc_nvls {
+    int rank, world, dev;
+    size_t size;  // mapping bytes (multiple of the multicast granularity)
+    CUmemGenericAllocationHandle mc, mem;
+    CUdeviceptr uc_va, mc_va;
+    int opened, bound;
+    int grid;
+};
+
+namespace {
+
+void* drv(const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess) return nullptr;
+    return fn;
+}
+#define DRV(name) reinterpret_cast<decltype(&name)>(drv(#name))
+
+int drv_err(const char* what, CUresult r) {
+    return lhc::set_error(LHC_ECOMM, "%s failed (CUresult %d)", what, (int)r);
+}
+
+void sock_addr(const char* name, sockaddr_un* a, socklen_t* len) {
+    memset(a, 0, sizeof(*a));
+    a->sun_family = AF_UNIX;
+    const size_t n = std::min(strlen(name), sizeof(a->sun_path) - 2);
+    memcpy(a->sun_path + 1, name, n);  // abstract namespace
+    *len = (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + n);
+}
+
+int send_fd(int sock, int fd) {
+    char byte = 0;
+    iovec io{&byte, 1};
+    char ctrl[CMSG_SPACE(sizeof(int))] = {};
+    msghdr m{};
+    m.msg_iov = &io;
+    m.msg_iovlen = 1;
+    m.msg_control = ctrl;
+    m.msg_controllen = sizeof(ctrl);
+    cmsghdr* c = CMSG_FIRSTHDR(&m);
+    c->cmsg_level = SOL_SOCKET;
+    c->cmsg_type = SCM_RIGHTS;
+    c->cmsg_len = CMSG_LEN(sizeof(int));
+    memcpy(CMSG_DATA(c), &fd, sizeof(int));
+    return sendmsg(sock, &m, 0) == 1 ? 0 : -1;
+}
+
+int recv_fd(int sock) {
+    char byte = 0;
+    iovec io{&byte, 1};
+    char ctrl[CMSG_SPACE(sizeof(int))] = {};
+    msghdr m{};
+    m.msg_iov = &io;
+    m.msg_iovlen = 1;
+    m.msg_control = ctrl;
+    m.msg_controllen = sizeof(ctrl);
+    if (recvmsg(sock, &m, 0) != 1) return -1;
+    cmsghdr* c = CMSG_FIRSTHDR(&m);
+    if (!c || c->cmsg_type != SCM_RIGHTS) return -1;
+    int fd = -1;
+    memcpy(&fd, CMSG_DATA(c), sizeof(int));
+    return fd;
+}
+
+}  // namespace
+
+using namespace lhc;
+
+extern "C" {
+
+int lhc_nvls_open(int rank, int world, const char* rendezvous, size_t bytes, lhc_nvls** out) {
+    if (!out || !rendezvous || !*rendezvous) return set_error(LHC_EINVAL, "NULL argument");
+    if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
+        return set_error(LHC_EINVAL, "world must be in [1, 8] and 0 <= rank < world");
+    if (bytes == 0) return set_error(LHC_EINVAL, "bytes must be > 0");
+    auto cuDeviceGet_ = DRV(cuDeviceGet);
+    auto cuMulticastGetGranularity_ = DRV(cuMulticastGetGranularity);
+    auto cuMulticastCreate_ = DRV(cuMulticastCreate);
+    auto cuMemExport_ = DRV(cuMemExportToShareableHandle);
+    auto cuMemImport_ = DRV(cuMemImportFromShareableHandle);
+    auto cuMulticastAddDevice_ = DRV(cuMulticastAddDevice);
+    if (!cuDeviceGet_ || !cuMulticastGetGranularity_ || !cuMulticastCreate_ || !cuMemExport_ ||
+        !cuMemImport_ || !cuMulticastAddDevice_)
+        return set_error(LHC_ECOMM, "multicast driver entry points unavailable");
+    int ord = 0;
+    cudaGetDevice(&ord);
+    cudaFree(nullptr);  // the runtime's primary context is current
+    CUdevice dev;
+    if (CUresult r = cuDeviceGet_(&dev, ord)) return drv_err("cuDeviceGet", r);
+    CUmulticastObjectProp prop{};
+    prop.numDevices = (unsigned)world;
+    prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    prop.size = bytes + kNvlsSig;
+    size_t gran = 0;
+    if (CUresult r = cuMulticastGetGranularity_(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED))
+        return drv_err("cuMulticastGetGranularity", r);
+    prop.size = (prop.size + gran - 1) / gran * gran;
+
+    CUmemGenericAllocationHandle mc = 0;
+    sockaddr_un addr;
+    socklen_t alen;
+    sock_addr(rendezvous, &addr, &alen);
+    if (rank == 0) {
+        if (CUresult r = cuMulticastCreate_(&mc, &prop)) return drv_err("cuMulticastCreate", r);
+        int fd = -1;
+        if (CUresult r = cuMemExport_(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0))
+            return drv_err("cuMemExportToShareableHandle", r);
+        int ls = socket(AF_UNIX, SOCK_STREAM, 0);
+        if (ls < 0 || bind(ls, (sockaddr*)&addr, alen) != 0 || listen(ls, world) != 0) {
+            if (ls >= 0) close(ls);
+            close(fd);
+            return set_error(LHC_ECOMM, "rendezvous socket '%s' unavailable", rendezvous);
+        }
+        for (int i = 1; i < world; i++) {
+            int c = accept(ls, nullptr, nullptr);
+            if (c < 0 || send_fd(c, fd) != 0) {
+                if (c >= 0) close(c);
+                close(ls);
+                close(fd);
+                return set_error(LHC_ECOMM, "sending the multicast handle failed");
+            }
+            close(c);
+        }
+        close(ls);
+        close(fd);
+    } else {
+        int s = -1;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (;;) {
+            s = socket(AF_UNIX, SOCK_STREAM, 0);
+            if (s >= 0 && connect(s, (sockaddr*)&addr, alen) == 0) break;
+            if (s >= 0) close(s);
+            s = -1;
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+                return set_error(LHC_ECOMM, "rank 0 did not open rendezvous '%s'", rendezvous);
+            std::this_thread::sleep_for(std::chrono::milliseconds(5));
+        }
+        const int fd = recv_fd(s);
+        close(s);
+        if (fd < 0) return set_error(LHC_ECOMM, "receiving the multicast handle failed");
+        CUresult r = cuMemImport_(&mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+        close(fd);
+        if (r) return drv_err("cuMemImportFromShareableHandle", r);
+    }
+    if (CUresult r = cuMulticastAddDevice_(mc, dev)) return drv_err("cuMulticastAddDevice", r);
+    lhc_nvls* h = new lhc_nvls();
+    h->rank = rank;
+    h->world = world;
+    h->dev = ord;
+    h->size = prop.size;
+    h->mc = mc;
+    h->opened = 1;
+    const void* fns[] = {(const void*)k_allreduce_nvls, (const void*)k_reduce_scatter_nvls,
+                         (const void*)k_allgather_nvls};
+    int per_sm = 4;
+    for (const void* f : fns) {
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, 256, 0);
+        per_sm = std::min(per_sm, n);
+    }
+    h->grid = std::max(1, per_sm) * num_sms();
+    *out = h;
+    return LHC_OK;
+}
+
+int lhc_nvls_bind(lhc_nvls* h, void** local_ptr, size_t* size) {
+    if (!h || !h->opened || h->bound) return set_error(LHC_EINVAL, "not an open, unbound NVLS handle");
+    auto cuMemCreate_ = DRV(cuMemCreate);
+    auto cuMulticastBindMem_ = DRV(cuMulticastBindMem);
+    auto cuMemAddressReserve_ = DRV(cuMemAddressReserve);
+    auto cuMemMap_ = DRV(cuMemMap);
+    auto cuMemSetAccess_ = DRV(cuMemSetAccess);
+    if (!cuMemCreate_ || !cuMulticastBindMem_ || !cuMemAddressReserve_ || !cuMemMap_ || !cuMemSetAccess_)
+        return set_error(LHC_ECOMM, "virtual memory driver entry points unavailable");
+    CUmemAllocationProp ap{};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = h->dev;
+    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // as the multicast object
+    if (CUresult r = cuMemCreate_(&h->mem, h->size, &ap, 0)) return drv_err("cuMemCreate", r);
+    if (CUresult r = cuMulticastBindMem_(h->mc, 0, h->mem, 0, h->size, 0)) return drv_err("cuMulticastBindMem", r);
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = h->dev;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (CUresult r = cuMemAddressReserve_(&h->uc_va, h->size, 0, 0, 0)) return drv_err("cuMemAddressReserve", r);
+    if (CUresult r = cuMemMap_(h->uc_va, h->size, 0, h->mem, 0)) return drv_err("cuMemMap", r);
+    if (CUresult r = cuMemSetAccess_(h->uc_va, h->size, &acc, 1)) return drv_err("cuMemSetAccess", r);
+    if (CUresult r = cuMemAddressReserve_(&h->mc_va, h->size, 0, 0, 0)) return drv_err("cuMemAddressReserve", r);
+    if (CUresult r = cuMemMap_(h->mc_va, h->size, 0, h->mc, 0)) return drv_err("cuMemMap(multicast)", r);
+    if (CUresult r = cuMemSetAccess_(h->mc_va, h->size, &acc, 1)) return drv_err("cuMemSetAccess(multicast)", r);
+    if (cudaMemset((void*)h->uc_va, 0, h->size) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+        return set_error(LHC_ECUDA, "clearing the NVLS buffer failed");
+    h->bound = 1;
+    if (local_ptr) *local_ptr = (void*)h->uc_va;
+    if (size) *size = h->size - kNvlsSig;
+    return LHC_OK;
+}
+
+static int nvls_launch(lhc_nvls* h, const void* fn, NvArgs& A, void* stream, const char* what) {
+    A.uc = (char*)h->uc_va;
+    A.mc = (char*)h->mc_va;
+    A.sig_uc = reinterpret_cast<uint32_t*>(h->uc_va + h->size - kNvlsSig);
+    A.sig_mc = reinterpret_cast<uint32_t*>(h->mc_va + h->size - kNvlsSig);
+    A.rank = h->rank;
+    A.world = h->world;
+    void* args[] = {(void*)&A};
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(h->grid), dim3(256), args, 0, (cudaStream_t)stream);
+    count_launch();
+    if (e != cudaSuccess) return set_error(LHC_ECUDA, "%s launch: %s", what, cudaGetErrorString(e));
+    return LHC_OK;
+}
+
+int sketch_allreduce_nvls(lhc_nvls* h, const lhc_params* p, void* stream) {
+    if (!h || !h->bound) return set_error(LHC_EINVAL, "NVLS handle not bound");
+    if (int rc = validate(p)) return rc;
+    size_t b, y, sb, sy, s, t;
+    layout(p, &b, &y, &sb, &sy, &s, &t);
+    const uint64_t units = (y + p->c * sizeof(float)) / 16;
+    if (units * 16 > h->size - kNvlsSig) return set_error(LHC_ECAPACITY, "NVLS buffer too small");
+    reset_launches();
+    NvArgs A{};
+    A.lo = units * h->rank / h->world;
+    A.hi = units * (h->rank + 1) / h->world;
+    A.y_unit = y / 16;
+    return nvls_launch(h, (const void*)k_allreduce_nvls, A, stream, "allreduce_nvls");
+}
+
+int sketch_reduce_scatter_nvls(lhc_nvls* h, const lhc_params* ps, uint64_t cap_items, void* stream) {
+    if (!h || !h->bound) return set_error(LHC_EINVAL, "NVLS handle not bound");
+    size_t slot, y, st, ga, sg, t;
+    if (int rc = shard_layout(ps, h->world, cap_items, &slot, &y, &st, &ga, &sg, &t)) return rc;
+    if (t > h->size - kNvlsSig) return set_error(LHC_ECAPACITY, "NVLS buffer too small for the shard layout");
+    reset_launches();
+    NvArgs A{};
+    A.slot_units = slot / 16;
+    A.y_unit = y / 16;
+    return nvls_launch(h, (const void*)k_reduce_scatter_nvls, A, stream, "reduce_scatter_nvls");
+}
+
+int sketch_allgather_decoded_nvls(lhc_nvls* h, const lhc_params* ps, uint64_t cap_items,
+                                  const uint32_t* idx, const float* val,
+                                  const unsigned long long* n_items, uint64_t shard_width, uint32_t d,
+                                  float* dense, void* stream) {
+    if (!h || !h->bound) return set_error(LHC_EINVAL, "NVLS handle not bound");
+    size_t slot, y, st, ga, sg, t;
+    if (int rc = shard_layout(ps, h->world, cap_items, &slot, &y, &st, &ga, &sg, &t)) return rc;
+    if (t > h->size - kNvlsSig) return set_error(LHC_ECAPACITY, "NVLS buffer too small for the shard layout");
+    if (!idx || !val || !n_items || !dense) return set_error(LHC_EINVAL, "NULL argument");
+    if (((uintptr_t)dense) & 15u) return set_error(LHC_EINVAL, "dense must be 16-byte aligned");
+    if (shard_width == 0 || shard_width % 4 || (uint64_t)(h->world - 1) * shard_width >= d)
+        return set_error(LHC_EINVAL, "shard_width must be a positive multiple of 4, every shard non-empty");
+    reset_launches();
+    if (h->world == 1) return LHC_OK;
+    NvArgs A{};
+    A.cap = (cap_items + 3) / 4 * 4;
+    A.gather_off = ga;
+    A.idx = idx;
+    A.val = val;
+    A.n_items = n_items;
+    A.dense = dense;
+    A.shard_width = shard_width;
+    A.d = d;
+    return nvls_launch(h, (const void*)k_allgather_nvls, A, stream, "allgather_nvls");
+}
+
+void lhc_nvls_destroy(lhc_nvls* h) {
+    if (!h) return;
+    auto cuMemUnmap_ = DRV(cuMemUnmap);
+    auto cuMemAddressFree_ = DRV(cuMemAddressFree);
+    auto cuMemRelease_ = DRV(cuMemRelease);
+    auto cuMulticastUnbind_ = DRV(cuMulticastUnbind);
+    auto cuDeviceGet_ = DRV(cuDeviceGet);
+    cudaDeviceSynchronize();
+    if (h->bound && cuMemUnmap_ && cuMemAddressFree_) {
+        cuMemUnmap_(h->uc_va, h->size);
+        cuMemUnmap_(h->mc_va, h->size);
+        cuMemAddressFree_(h->uc_va, h->size);
+        cuMemAddressFree_(h->mc_va, h->size);
+    }
+    CUdevice dev;
+    if (h->bound && cuMulticastUnbind_ && cuDeviceGet_ && !cuDeviceGet_(&dev, h->dev))
+        cuMulticastUnbind_(h->mc, dev, 0, h->size);
+    if (cuMemRelease_) {
+        if (h->bound) cuMemRelease_(h->mem);
+        if (h->opened) cuMemRelease_(h->mc);
+    }
+    delete h;
+}
+
+}  // extern "C"

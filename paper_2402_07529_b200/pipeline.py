@@ -15,11 +15,11 @@ class Sketch:
     """S(X) = [Y, B] (Alg. 1) in one device buffer laid out as
     [bitmap | counters | signals] (lhc_comm_layout), usable as an all-reduce buffer."""
 
-    def __init__(self, p: L.lhc_params, device="cuda"):
+    def __init__(self, p: L.lhc_params, device="cuda", buf: torch.Tensor | None = None):
         self.p = p
         b_off, y_off, s_off, total = L.lhc_comm_layout(p)
         # zero-initialised: the signal slots must start at zero (include/lhc.h)
-        self.buf = torch.zeros(total, dtype=torch.uint8, device=device)
+        self.buf = torch.zeros(total, dtype=torch.uint8, device=device) if buf is None else buf
         self.bitmap = self.buf[b_off:b_off + p.words * 4].view(torch.int32)
         self.counters = self.buf[y_off:y_off + int(p.c) * 4].view(torch.float32)
 
@@ -132,6 +132,62 @@ class PeerComm:
             pass
 
 
+class NvlsBuffer:
+    """A zeroed device buffer bound to an NVSwitch multicast object shared by the
+    ranks of a process group (lhc_nvls_open / lhc_nvls_bind); construction is
+    collective.  ``buf`` is the local (unicast) view."""
+
+    _serial = 0
+
+    def __init__(self, nbytes: int, group=None, device=None):
+        import os
+
+        import torch.distributed as dist
+
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        NvlsBuffer._serial += 1
+        name = [f"lhc-nvls-{os.getpid()}-{NvlsBuffer._serial}"]
+        dist.broadcast_object_list(name, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        self.handle = L.lhc_nvls_open(self.rank, self.world, name[0], nbytes)
+        dist.barrier(group=group)        # every device added before any binds
+        ptr, size = L.lhc_nvls_bind(self.handle)
+        dist.barrier(group=group)
+        self.buf = L.device_bytes(ptr, size, device)
+
+    def close(self):
+        if self.handle:
+            torch.cuda.synchronize()
+            self.buf = None
+            L.lhc_nvls_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NvlsComm:
+    """In-switch all-reduce of a Sketch (sketch_allreduce_nvls): drop-in for PeerComm."""
+
+    def __init__(self, p: L.lhc_params, group=None, device=None):
+        self.p = p
+        _, _, _, total = L.lhc_comm_layout(p)
+        self.nvls = NvlsBuffer(total, group, device)
+        self.rank, self.world = self.nvls.rank, self.nvls.world
+        self.sketch = Sketch(p, buf=self.nvls.buf[:total])
+
+    def allreduce(self, stream=None):
+        L.sketch_allreduce_nvls(self.nvls.handle, self.p, stream)
+
+    def close(self):
+        self.nvls.close()
+
+
 class LosslessAllReduce:
     """One step of Alg. 1 for the workers a rank holds: compress every local
     gradient into the rank's sketch (homomorphic accumulation), make the
@@ -207,7 +263,8 @@ class ShardedAllReduce:
     one process, which then decodes every shard itself)."""
 
     def __init__(self, plan, k: int = 3, L_rows: int = 1024, seed: int = 0, cap_cand: int = 0,
-                 local_workers: int = 1, per_worker: bool = True, group=None, device=None):
+                 local_workers: int = 1, per_worker: bool = True, group=None, device=None,
+                 comm: str = "p2p"):
         import torch.distributed as dist
 
         self.plan = plan
@@ -223,7 +280,15 @@ class ShardedAllReduce:
         self.cap = int(cap_cand) or int(1.25 * s.n_cand_expected) + 4096
         self.cap = min(self.cap, plan.width)
         self.slot_bytes, self.y_off, total = L.lhc_shard_layout(self.ps[0], self.world, self.cap)
-        self.buf = torch.zeros(total, dtype=torch.uint8, device=device)
+        if comm not in ("p2p", "nvls"):
+            raise ValueError("comm must be 'p2p' or 'nvls'")
+        self.comm = comm if self.world > 1 else "none"
+        self.nvls = None
+        if self.comm == "nvls":   # the sharded buffer lives in the multicast-bound memory
+            self.nvls = NvlsBuffer(total, group, device)
+            self.buf = self.nvls.buf[:total]
+        else:
+            self.buf = torch.zeros(total, dtype=torch.uint8, device=device)
         words = self.ps[0].words
         self.slots = [_SlotSketch(self.ps[q], self.buf, q * self.slot_bytes, self.y_off, words)
                       for q in range(plan.shards)]
@@ -246,7 +311,7 @@ class ShardedAllReduce:
             self.decoders[q] = dec
         self.decoder = self.decoders[self.owned[0]]
         self.handle = None
-        if self.world > 1:
+        if self.comm == "p2p":
             torch.cuda.synchronize()
             handle, offset = L.lhc_ipc_handle(self.buf)
             handles, offsets = exchange_handles(handle, offset, group)
@@ -305,20 +370,36 @@ class ShardedAllReduce:
                 L.sketch_aggregate(self.ps[q], [b[q].bitmap for b in self.worker_bufs],
                                    [b[q].counters for b in self.worker_bufs],
                                    self.slots[q].bitmap, self.slots[q].counters, stream)
-        if self.world > 1:
-            L.sketch_reduce_scatter(self.handle, stream)
+        self.reduce_scatter(stream)
         for q in self.owned:
             self.decoders[q](self.slots[q], stream)
         dec = self.decoder
-        if self.world > 1:
+        self.allgather(stream)
+        return dec
+
+    def reduce_scatter(self, stream=None):
+        if self.comm == "p2p":
+            L.sketch_reduce_scatter(self.handle, stream)
+        elif self.comm == "nvls":
+            L.sketch_reduce_scatter_nvls(self.nvls.handle, self.ps[0], self.cap, stream)
+
+    def allgather(self, stream=None):
+        dec = self.decoder
+        if self.comm == "p2p":
             L.sketch_allgather_decoded(self.handle, dec.idx, dec.val, dec.stats, self.plan.width,
                                        self.plan.d, self.dense, stream)
-        return dec
+        elif self.comm == "nvls":
+            L.sketch_allgather_decoded_nvls(self.nvls.handle, self.ps[0], self.cap, dec.idx,
+                                            dec.val, dec.stats, self.plan.width, self.plan.d,
+                                            self.dense, stream)
 
     def close(self):
         if self.handle:
             L.lhc_comm_destroy(self.handle)
             self.handle = None
+        if getattr(self, "nvls", None) is not None:
+            self.nvls.close()
+            self.nvls = None
 
     def __del__(self):
         try:

@@ -20,7 +20,7 @@ import torch.distributed as dist  # noqa: E402
 from lhc_inputs import config  # noqa: E402
 
 
-def sharded(name, law, steps, rank, world, dev):
+def sharded(name, law, steps, rank, world, dev, comm="p2p"):
     """NEXT-2: reduce-scatter of per-shard sub-sketches, decode of the own shard,
     all-gather of the decoded lists.  Every rank checks its shard against the
     oracle on that coordinate range; all ranks must hold identical dense sums."""
@@ -33,7 +33,7 @@ def sharded(name, law, steps, rank, world, dev):
     plan = shard_plan(wl.d, world, wl.density, wl.workers)
     mine = [w for w in range(wl.workers) if w % world == rank]
     xs = [torch.from_numpy(wl.dense(w)).to(dev) for w in mine]
-    run = lhc.ShardedAllReduce(plan, seed=0x5BA4D, local_workers=len(xs), device=dev)
+    run = lhc.ShardedAllReduce(plan, seed=0x5BA4D, local_workers=len(xs), device=dev, comm=comm)
     for _ in range(steps):
         dec = run.step(xs)
     torch.cuda.synchronize()
@@ -70,7 +70,7 @@ def sharded(name, law, steps, rank, world, dev):
     total = np.sum(np.stack(xs_all).astype(np.float64), axis=0)
     if law == "dyadic" and st["success"]:
         ok &= np.array_equal(dense[lo:hi].astype(np.float64), total[lo:hi])
-    print(f"mgpu-sharded {name} world={world} rank={rank} n_cand={n} rounds={st['rounds']} "
+    print(f"mgpu-sharded[{comm}] {name} world={world} rank={rank} n_cand={n} rounds={st['rounds']} "
           f"ok={ok}", flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
@@ -93,8 +93,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    if mode == "sharded":
-        ok = sharded(name, law, steps, rank, world, dev)
+    if mode in ("sharded", "sharded-nvls"):
+        ok = sharded(name, law, steps, rank, world, dev, "nvls" if mode == "sharded-nvls" else "p2p")
         dist.destroy_process_group()
         sys.exit(0 if ok else 1)
     import paper_2402_07529_b200 as lhc
@@ -106,7 +106,7 @@ def main():
     p = lhc.params(wl.d, s.m, s.c, 3, 0, 1024, 0x1DC0DE)
     mine = [w for w in range(wl.workers) if w % world == rank]
     xs = [torch.from_numpy(wl.dense(w)).to(dev) for w in mine]
-    comm = lhc.PeerComm(p)
+    comm = lhc.NvlsComm(p) if mode == "nvls" else lhc.PeerComm(p)
     run = lhc.LosslessAllReduce(p, min(wl.d, int(s.n_cand_expected * 1.5) + 4096),
                                 local_workers=len(xs), comm=comm, device=dev)
     for _ in range(steps):  # repeated steps exercise the barrier epochs

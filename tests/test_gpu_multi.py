@@ -38,3 +38,18 @@ def test_sharded_decode_parity(world, name, law):
            os.path.join(ROOT, "tests", "mgpu_worker.py"), name, law, "3", "sharded"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("mode", ["nvls", "sharded-nvls"])
+@pytest.mark.parametrize("name,law", [("tiny", "dyadic"), ("ncf", "gauss")])
+def test_nvls_parity(world, mode, name, law):
+    """NEXT-2: in-switch aggregation through an NVSwitch multicast object, for the
+    replicated all-reduce and for the sharded reduce-scatter / all-gather."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29535",
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), name, law, "3", mode]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

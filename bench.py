@@ -608,6 +608,20 @@ def main():
                          "frac": ach / peak, "bytes_per_launch": int(byts),
                          "avg_launch_us": ms_l * 1e3, "launches_per_step": nl,
                          "us_per_step": ms_l * 1e3 * nl}
+    # the peel's own bound: L2 atomics (key inserts when the state is built in-kernel,
+    # one claim per frontier entry, two updates per other cell of a peeled candidate)
+    # against the measured ATOM.ADD.64-with-return peak (tools/atomic_peak.cu)
+    if "k_peel" in kernels:
+        pd = p_dec
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+        insert = 3 * n_c if 16 * int(pd.c) <= l2 // 2 else 0
+        n_atom = insert + stats.get("entries", 0) + 2 * (3 - 1) * stats["n_peeled"]
+        t_peel = kernels["k_peel"]["avg_launch_us"] * 1e-6
+        kernels["k_peel"]["l2_atomics"] = {
+            "count": int(n_atom), "achieved": n_atom / t_peel / 1e9, "peak": 122.0,
+            "unit": "G atomics/s", "frac": n_atom / t_peel / 1e9 / 122.0,
+            "peak_source": "tools/atomic_peak.cu: random ATOM.ADD.64 with return, 64 MB footprint",
+            "rounds": stats["rounds"], "entries": stats.get("entries", 0)}
     dom = max(kernels, key=lambda k: kernels[k]["us_per_step"])
     roofline = dict(kernels[dom])
     roofline.update({"kernel": dom, "traffic": None,
@@ -616,6 +630,8 @@ def main():
     roofline = {k: roofline[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic",
                                          "kernel", "bytes_per_launch", "avg_launch_us",
                                          "peak_source")}
+    if "l2_atomics" in kernels[dom]:
+        roofline["l2_atomics"] = kernels[dom]["l2_atomics"]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -74,7 +74,7 @@ typedef struct lhc_stats {
     uint32_t rounds;   /* synchronous peeling rounds that peeled something ("iterations")    */
     int32_t success;   /* 1 iff n_peeled == n_cand and no overflow (lossless)        */
     int32_t overflow;  /* 1 iff n_cand > cap_cand: outputs truncated, nothing peeled         */
-    uint32_t _reserved;
+    uint32_t entries;  /* frontier entries the rounds processed (F0 included; one claim each) */
 } lhc_stats;
 
 enum {

@@ -64,7 +64,7 @@ class lhc_stats(ctypes.Structure):
         ("rounds", ctypes.c_uint32),
         ("success", ctypes.c_int32),
         ("overflow", ctypes.c_int32),
-        ("_reserved", ctypes.c_uint32),
+        ("entries", ctypes.c_uint32),
     ]
 
 
@@ -413,4 +413,4 @@ def read_stats(stats: torch.Tensor) -> dict:
     raw = bytes(stats.cpu().numpy().tobytes())
     s = lhc_stats.from_buffer_copy(raw)
     return dict(n_cand=int(s.n_cand), n_peeled=int(s.n_peeled), rounds=int(s.rounds),
-                success=bool(s.success), overflow=bool(s.overflow))
+                success=bool(s.success), overflow=bool(s.overflow), entries=int(s.entries))

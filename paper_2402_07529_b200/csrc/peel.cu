@@ -524,6 +524,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
         stats->n_peeled = n_peeled;
         stats->rounds = rounds;
         stats->success = (uint64_t)n_peeled == n_c ? 1 : 0;
+        stats->entries = f_end;  // every entry appended was processed by a round
         ctrl->rounds_dbg = rounds;
     }
 }
@@ -559,6 +560,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
             stats->n_peeled = 0;
             stats->rounds = 0;
             stats->success = 0;
+            stats->entries = 0;
         }
         return;
     }

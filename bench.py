@@ -504,41 +504,83 @@ def main():
             e2e = None
 
         # the same through the COO boundary (the gradients are sparse): pinned host
-        # (idx, val) per worker -> H2D -> LosslessAllReduce.step_coo -> the aggregate's
-        # candidate list (idx, val) and stats D2H (cap entries, no host sync inside)
+        # (idx, val) per worker -> H2D -> step_coo -> the aggregate's candidate list
+        # (idx, val) and stats D2H (cap entries, no host sync inside).  Steps are
+        # pipelined the way a training loop would run them: two engines alternate, the
+        # H2D of step i+1 and the D2H of step i run on their own streams while step i
+        # / i+1 computes (PCIe is full duplex); every step still moves all its bytes.
         coo_host = [wl.coo(w) for w in my_workers]
         if sharded:   # per-shard lists with shard-relative indices (split once on the host)
             coo_host = [c for i, v in coo_host for c in run.split_coo(i, v)]
         pin_i = [torch.from_numpy(i.view(np.int32)).pin_memory() for i, _ in coo_host]
         pin_v = [torch.from_numpy(v).pin_memory() for _, v in coo_host]
-        dev_i = [torch.empty_like(t, device=dev) for t in pin_i]
-        dev_v = [torch.empty_like(t, device=dev) for t in pin_v]
-        pairs = list(zip(dev_i, dev_v))
-        items = [pairs[w * G:(w + 1) * G] for w in range(len(my_workers))] if sharded else pairs
+        if sharded:
+            run_b = lhc.ShardedAllReduce(run.plan, seed=SEED, local_workers=len(xs),
+                                         per_worker=not args.fuse_local, device=dev, comm=args.comm)
+        else:
+            comm_b = None
+            if world > 1 and args.comm == "p2p":
+                comm_b = lhc.PeerComm(p)
+            elif world > 1 and args.comm == "nvls":
+                comm_b = lhc.NvlsComm(p)
+            run_b = lhc.LosslessAllReduce(p, cap, local_workers=len(xs),
+                                          per_worker=not args.fuse_local, comm=comm_b, device=dev)
+        engines = [run, run_b]
+        ins, items_k, outs = [], [], []
         cap_ = run.decoder.cap
-        oi = torch.empty(cap_, dtype=torch.int32).pin_memory()
-        ov = torch.empty(cap_, dtype=torch.float32).pin_memory()
-        ost = torch.empty(32, dtype=torch.uint8).pin_memory()
+        for k in range(2):
+            dev_i = [torch.empty_like(t, device=dev) for t in pin_i]
+            dev_v = [torch.empty_like(t, device=dev) for t in pin_v]
+            ins.append((dev_i, dev_v))
+            pairs = list(zip(dev_i, dev_v))
+            items_k.append([pairs[w * G:(w + 1) * G] for w in range(len(my_workers))]
+                           if sharded else pairs)
+            outs.append((torch.empty(cap_, dtype=torch.int32).pin_memory(),
+                         torch.empty(cap_, dtype=torch.float32).pin_memory(),
+                         torch.empty(32, dtype=torch.uint8).pin_memory()))
+        s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        s_comp = stream
+        ev = {n: [torch.cuda.Event() for _ in range(2)] for n in ("in", "comp", "out")}
+        for k in range(2):
+            for n in ev:
+                ev[n][k].record(s_comp)
 
-        def e2e_coo_step():
-            for a, b in zip(pin_i + pin_v, dev_i + dev_v):
-                b.copy_(a, non_blocking=True)
-            d = run.step_coo(items)
-            oi.copy_(d.idx[:cap_], non_blocking=True)
-            ov.copy_(d.val[:cap_], non_blocking=True)
-            ost.copy_(d.stats, non_blocking=True)
+        def e2e_coo_step(i):
+            k = i % 2
+            s_in.wait_event(ev["comp"][k])            # step i-2 no longer reads ins[k]
+            with torch.cuda.stream(s_in):
+                for a, b_ in zip(pin_i + pin_v, ins[k][0] + ins[k][1]):
+                    b_.copy_(a, non_blocking=True)
+                ev["in"][k].record(s_in)
+            s_comp.wait_event(ev["in"][k])
+            s_comp.wait_event(ev["out"][k])           # step i-2's results have left
+            d = engines[k].step_coo(items_k[k], stream=s_comp)
+            ev["comp"][k].record(s_comp)
+            s_out.wait_event(ev["comp"][k])
+            with torch.cuda.stream(s_out):
+                oi, ov, ost = outs[k]
+                oi.copy_(d.idx[:cap_], non_blocking=True)
+                ov.copy_(d.val[:cap_], non_blocking=True)
+                ost.copy_(d.stats, non_blocking=True)
+                ev["out"][k].record(s_out)
 
-        for _ in range(2):
-            e2e_coo_step()
+        for i in range(2):
+            e2e_coo_step(i)
+        torch.cuda.synchronize()
         barrier()
-        e0.record(stream)
-        for _ in range(n_e2e):
-            e2e_coo_step()
-        e1.record(stream)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s_in)
+        for i in range(n_e2e):
+            e2e_coo_step(i)
+        e1.record(s_out)
+        torch.cuda.synchronize()
         barrier()
         c_ms = torch.tensor([e0.elapsed_time(e1) / n_e2e], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(c_ms, op=dist.ReduceOp.MAX)
+        # the last step's results equal a serial step's (same inputs)
+        st_b = lhc.read_stats(outs[(n_e2e - 1) % 2][2])
         # headline e2e: the sparse (COO) boundary, the natural host form of these
         # gradients; the dense-boundary measurement is kept beside it
         dense_e2e = e2e
@@ -548,8 +590,15 @@ def main():
                "path": "pinned host COO (idx, val) per worker -> H2D -> "
                        f"{type(run).__name__}.step_coo -> candidate list (idx, val) + stats D2H"
                        + (" (own shard's list; every rank also holds the dense sum)"
-                          if sharded else ""),
+                          if sharded else "")
+                       + "; steps pipelined over 3 streams (H2D / compute / D2H), 2 engines",
+               "decode_ok": bool(st_b["success"] and st_b["n_cand"] == stats["n_cand"]),
                "dense": dense_e2e}
+        for eng in engines[1:]:
+            if getattr(eng, "comm", None) is not None and hasattr(eng.comm, "close"):
+                eng.comm.close()
+            if hasattr(eng, "close"):
+                eng.close()
 
     trace('roofline')
     # ---- roofline: every step of the path against its bound; the dominant one ----

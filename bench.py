@@ -376,7 +376,8 @@ def main():
     trace('timed')
     # ---- timed region: K steps, per-step events, L2 flushed between steps ----
     clocks = ClockSampler(local_rank)
-    phase = {"compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "query": 0.0, "peel": 0.0,
+    phase = {"clear": 0.0, "compress": 0.0, "aggregate": 0.0, "allreduce": 0.0, "query": 0.0,
+             "peel": 0.0,
              "allgather": 0.0}
     compress_launch_ms = []
     launches = [0]
@@ -393,6 +394,8 @@ def main():
             if name == "compress1":
                 compress_launch_ms.append(dt)
                 phase["compress"] += dt
+            elif name == "compress0":
+                phase["clear"] += dt
             elif name in phase:
                 phase[name] += dt
             prev = e
@@ -648,6 +651,8 @@ def main():
             # peel + finalize, and the dense output (zeroed, then the values at candidates)
             "k_peel": (16 * int(p.c) + 9 * n_c + 4 * wl.d, 1, per_step_ms["peel"], hbm, "hbm"),
         }
+    n_clr = W_loc if run.per_worker else 1
+    kern["k_clear"] = (n_clr * (S_all if sharded else S), 1, per_step_ms["clear"], hbm, "hbm")
     kernels = {}
     for name, (byts, nl, ms_l, peak, bound) in kern.items():
         if nl == 0 or ms_l <= 0:
@@ -671,9 +676,20 @@ def main():
             "unit": "G atomics/s", "frac": n_atom / t_peel / 1e9 / 122.0,
             "peak_source": "tools/atomic_peak.cu: random ATOM.ADD.64 with return, 64 MB footprint",
             "rounds": stats["rounds"], "entries": stats.get("entries", 0)}
+    # measured DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum of
+    # one `ncu --set full` capture of this workload at N = 1, profiles/traffic.json)
+    traffic = {}
+    try:
+        tf = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        if world == 1 and not sharded and args.comm == "p2p":
+            traffic = tf.get(wl.name + ("-bitmap" if kb == INDEX_BITMAP else ""), {})
+    except Exception:
+        pass
+    for name in kernels:
+        kernels[name]["traffic"] = traffic.get(name)
     dom = max(kernels, key=lambda k: kernels[k]["us_per_step"])
     roofline = dict(kernels[dom])
-    roofline.update({"kernel": dom, "traffic": None,
+    roofline.update({"kernel": dom,
                      "peak_source": hbm_src if roofline["bound"] == "hbm" else
                      "B200_PROFILING.md measured peer copy 770 GB/s"})
     roofline = {k: roofline[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic",

@@ -297,33 +297,41 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
     const uint64_t nv = n / 4;
     const uint4* src_i = reinterpret_cast<const uint4*>(A.idx);
     const uint4* src_v = reinterpret_cast<const uint4*>(A.val);
+    // the first half of the grid pushes over NVLink while the second half zeroes
+    // the local dense ranges in HBM (the two transfers overlap)
+    const uint32_t half = gridDim.x / 2;
+    const bool pusher = blockIdx.x < half || half == 0;
+    const uint64_t rtid = (pusher ? blockIdx.x : blockIdx.x - half) * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t rstride = (uint64_t)(half ? half : gridDim.x) * blockDim.x;
+    if (pusher) {
 #pragma unroll 1
-    for (int dd = 1; dd < G; dd++) {
-        const int q = (A.rank + dd) % G;
-        uint32_t* slot = reinterpret_cast<uint32_t*>(A.gather[q] + ((uint64_t)par * G + A.rank) * A.cap);
-        uint4* di = reinterpret_cast<uint4*>(slot);
-        uint4* dv = reinterpret_cast<uint4*>(slot + A.cap);
-        for (uint64_t u = gtid; u < nv; u += gstride) {
-            const uint4 a = __ldcg(src_i + u), b = __ldcg(src_v + u);
-            di[u] = a;
-            dv[u] = b;
+        for (int dd = 1; dd < G; dd++) {
+            const int q = (A.rank + dd) % G;
+            uint32_t* slot = reinterpret_cast<uint32_t*>(A.gather[q] + ((uint64_t)par * G + A.rank) * A.cap);
+            uint4* di = reinterpret_cast<uint4*>(slot);
+            uint4* dv = reinterpret_cast<uint4*>(slot + A.cap);
+            for (uint64_t u = rtid; u < nv; u += rstride) {
+                const uint4 a = __ldcg(src_i + u), b = __ldcg(src_v + u);
+                di[u] = a;
+                dv[u] = b;
+            }
+            for (uint64_t i = 4 * nv + rtid; i < n; i += rstride) {
+                slot[i] = __ldcg(A.idx + i);
+                slot[A.cap + i] = __float_as_uint(__ldcg(A.val + i));
+            }
+            if (rtid == 0) A.sig[q][kGatherCountSlot + par * kMaxRanks + A.rank] = (uint32_t)n;
         }
-        for (uint64_t i = 4 * nv + gtid; i < n; i += gstride) {
-            slot[i] = __ldcg(A.idx + i);
-            slot[A.cap + i] = __float_as_uint(__ldcg(A.val + i));
-        }
-        if (gtid == 0) A.sig[q][kGatherCountSlot + par * kMaxRanks + A.rank] = (uint32_t)n;
     }
-    // zero the peers' shard ranges [0, lo) and [hi, d) of the local dense output
-    // meanwhile (lo, hi multiples of 4 unless hi = d)
-    {
+    if (!pusher || half == 0) {
+        // zero the peers' shard ranges [0, lo) and [hi, d) of the local dense output
+        // (lo, hi multiples of 4 unless hi = d)
         const uint64_t lo = (uint64_t)A.rank * A.shard_width;
         const uint64_t hi = min((uint64_t)A.d, lo + A.shard_width);
         float4* d4 = reinterpret_cast<float4*>(A.dense);
         const uint64_t a4 = lo / 4, b4 = hi / 4, e4 = A.d / 4, own4 = b4 - a4;
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (uint64_t u = gtid; u < e4 - own4; u += gstride) __stcs(d4 + (u < a4 ? u : u + own4), z);
-        for (uint64_t i = max(hi, 4 * e4) + gtid; i < A.d; i += gstride) A.dense[i] = 0.f;
+        for (uint64_t u = rtid; u < e4 - own4; u += rstride) __stcs(d4 + (u < a4 ? u : u + own4), z);
+        for (uint64_t i = max(hi, 4 * e4) + rtid; i < A.d; i += rstride) A.dense[i] = 0.f;
     }
     sh_barrier<G>(grid, A, epoch + 1);
 #pragma unroll 1

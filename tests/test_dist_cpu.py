@@ -67,6 +67,37 @@ def _worker(rank, world, port, q):
         assert np.array_equal(Yt.numpy(), Yref)
         dec = oracle.decompress(p, Bor, Yt.numpy())
         assert dec.stats.success and np.array_equal(dec.dense, ref.dense)
+
+        # sharded decode protocol (NEXT-2a, reading R23) with the oracle standing in
+        # for the kernels: per-shard sketches, reduce-scatter (sum/OR, keep the own
+        # shard), decode the own shard, all-gather the decoded lists, assemble
+        from paper_2402_07529_b200.sizing import shard_plan
+
+        plan = shard_plan(wl.d, world, wl.density, wl.workers)
+        ps = [oracle.params(plan.shard_d(r), plan.shard_m(r), plan.sizing.c, 3, 0, 1024, 77)
+              for r in range(world)]
+        lo, hi = plan.bounds(rank)
+        mine = {}
+        for r in range(world):
+            Br, Yr = oracle.empty_sketch(ps[r])
+            a, b = plan.bounds(r)
+            for w in owned_workers(wl.workers, rank, world):
+                oracle.compress_dense(ps[r], wl.dense(w)[a:b], Br, Yr)
+            Yt = torch.from_numpy(Yr.copy())
+            dist.all_reduce(Yt)                      # reduce (rank r keeps shard r)
+            Bs = [torch.zeros(len(Br), dtype=torch.int32) for _ in range(world)]
+            dist.all_gather(Bs, torch.from_numpy(Br.view(np.int32).copy()))
+            if r == rank:
+                Bo = np.bitwise_or.reduce(np.stack([t.numpy().view(np.uint32) for t in Bs]), axis=0)
+                mine = oracle.decompress(ps[r], Bo, Yt.numpy())
+        assert mine.stats.success
+        lists = [None] * world
+        dist.all_gather_object(lists, (mine.cand.astype(np.int64).tolist(), mine.val.tolist()))
+        dense = np.zeros(wl.d)
+        for r, (idx, val) in enumerate(lists):
+            dense[plan.bounds(r)[0] + np.asarray(idx, dtype=np.int64)] = val
+        exact = np.sum(np.stack([wl.dense(w).astype(np.float64) for w in range(wl.workers)]), axis=0)
+        assert np.array_equal(dense, exact)              # lossless (dyadic law: exact sums)
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))

@@ -184,3 +184,27 @@ def shard_plan(d: int, shards: int, density: float, workers: int, **kw) -> Shard
     if (shards - 1) * width >= d:
         raise ValueError(f"d={d} is too small for {shards} non-empty shards of {width}")
     return ShardPlan(d, shards, width, size_workload(width, density, workers, **kw))
+
+
+# ---- NEXT-4: the paper's optimal Bloom configuration --------------
+
+K_MAX = 8  # probes / hashes the kernels support (include/lhc.h)
+
+
+def size_paper_optimal(d: int, n: float, C: int = 32, gamma: float = GAMMA_DEFAULT, k: int = 3,
+                       L: int = 1024) -> Sizing:
+    """The §3.3 construction: false-positive rate eps* = (ln^2 2 * gamma * C * lambda)^-1
+    with lambda n = N - n, a Bloom filter of n/ln2 * log2(1/eps*) bits
+    hashing every nonzero to log2(1/eps*) bits (rounded, at most K_MAX), and
+    c = gamma (n + eps (N - n)) counters with eps the realised false-positive
+    rate of the partitioned filter.  Rounded to the kernels' multiples (k_B L, k L)."""
+    n = max(float(n), 1.0)
+    lam = max((d - n) / n, 1e-12)
+    eps_star = optimal_eps(C, lam, gamma)
+    lg = math.log2(1.0 / eps_star) if eps_star < 1.0 else 0.0
+    kb = max(1, min(K_MAX, int(round(lg))))
+    m = max(kb * L, _round_up(n / math.log(2) * max(lg, 1.0), kb * L))
+    eps = bloom_fp_rate(m, n, kb)
+    nc = n + eps * (d - n)
+    c = max(k * L, _round_up(gamma * nc, k * L))
+    return Sizing(d, m, c, k, kb, L, n, eps, nc, gamma)

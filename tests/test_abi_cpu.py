@@ -176,3 +176,29 @@ def test_shard_layout(lhc):
     assert L.sketch_reduce_scatter(None, None) == lhc._lib.LHC_EINVAL
     assert L.sketch_allgather_decoded(None, None, None, None, 4096, 10_000, None, None) == \
         lhc._lib.LHC_EINVAL
+
+
+# ---------------------------------------- NEXT-4: paper-optimal Bloom sizing --
+
+@pytest.mark.parametrize("density", [0.10, 0.30, 0.696])
+def test_paper_optimal_sizing(lhc, density):
+    """k_B = log2(1/eps*) probes, m = n/ln2 log2(1/eps*) bits,
+    c = gamma n (1 + eps lambda); the realised partitioned-filter false-positive rate
+    is close to eps*, and the total stays below 1.6 S_min."""
+    from paper_2402_07529_b200 import sizing
+
+    d = 10_000_000
+    n = d * density
+    s = sizing.size_paper_optimal(d, n, C=32, gamma=1.23)
+    lam = (d - n) / n
+    eps_star = sizing.optimal_eps(32, lam, 1.23)
+    lg = math.log2(1 / eps_star)
+    assert s.k_bloom == max(1, min(8, round(lg)))
+    assert s.m % (s.k_bloom * 1024) == 0 and s.c % (3 * 1024) == 0
+    assert abs(s.m - n / math.log(2) * lg) <= s.k_bloom * 1024
+    assert 0.5 * eps_star < s.eps < 2.0 * eps_star
+    assert abs(s.c - 1.23 * n * (1 + s.eps * lam)) <= 3 * 1024
+    S = s.m + 32 * s.c
+    assert S < 1.6 * sizing.s_min_bits(n, lam, 32)
+    p = lhc.params(d, s.m, s.c, 3, s.k_bloom, 1024, 1)
+    assert lhc.lhc_validate(p)

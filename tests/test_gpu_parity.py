@@ -448,3 +448,47 @@ def test_compress_batch_chained_and_repeated(lhc, ora):
         B, Y = ora.aggregate([a for a, _ in parts], [b for _, b in parts])
         assert np.array_equal(U(sks[r].bitmap), B)
         assert np.array_equal(F(sks[r].counters), Y)
+
+
+# ------------------------------- generic k / k_B (run-time k kernels, NEXT-4) --
+
+@pytest.mark.parametrize("k,kb", [(2, 1), (4, 5), (3, 7), (5, 0)])
+@pytest.mark.parametrize("law", ["dyadic", "gauss"])
+def test_generic_k_and_probes(lhc, ora, k, kb, law):
+    """The run-time-k kernels (k != 3 or k_B != 3): bitmaps, candidates, flags and
+    rounds exact, values exact/tol — including k = 2 below its peeling threshold,
+    where most values come from the median (here: mean) fallback."""
+    d, nnz, W = 300_000, 6_000, 2
+    s = lhc.size_workload(d, nnz / d, W, k=k, k_bloom=kb)
+    p = gpu_params(lhc, d, s.m, s.c, k=k, kb=kb, seed=0x6E + 16 * k + kb)
+    op = ora_params(ora, p)
+    xs = make_workers(d, nnz, W, 3 + k, law)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(op, xs)
+    assert np.array_equal(U(run.sketch.bitmap), B)
+    assert_values(F(run.sketch.counters), Y, law == "dyadic")
+    compare_decode(ora, dec, ref, law == "dyadic")
+
+
+@pytest.mark.parametrize("density", [0.10, 0.30])
+def test_paper_optimal_bloom_pipeline(lhc, ora, density):
+    """NEXT-4: the paper's eps*-optimal Bloom filter (k_B = log2 1/eps* probes)
+    end to end against the oracle, one worker at the given density."""
+    from paper_2402_07529_b200.sizing import size_paper_optimal
+
+    d = 500_000
+    nnz = int(d * density)
+    s = size_paper_optimal(d, nnz, C=32, gamma=1.30)
+    assert s.k_bloom != 3
+    p = gpu_params(lhc, d, s.m, s.c, kb=s.k_bloom, seed=0x0B7 + nnz)
+    op = ora_params(ora, p)
+    xs = make_workers(d, nnz, 1, 21, "dyadic")
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=1)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(op, xs)
+    assert np.array_equal(U(run.sketch.bitmap), B)
+    st = compare_decode(ora, dec, ref, True)
+    assert st["success"]

@@ -68,7 +68,11 @@ void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* co
 // Zero a sketch with L2 evict-last stores: the lines stay L2-resident for the
 // compress reductions that follow (a cold sketch costs one random DRAM sector
 // read per first touch).
-// clear up to kMaxBatch sketches: blockIdx.y = sketch
+// clear up to kMaxBatch sketches: blockIdx.y = sketch.  L2 policy of the zero stores
+// (LHC_CLEAR_POLICY): 0 evict-last, 1 normal, 2 evict-first
+#ifndef LHC_CLEAR_POLICY
+#define LHC_CLEAR_POLICY 0
+#endif
 struct ClearBatch {
     uint4* counters[kMaxBatch];
     uint32_t* bitmap[kMaxBatch];
@@ -76,7 +80,13 @@ struct ClearBatch {
 __global__ void __launch_bounds__(256) k_clear(const __grid_constant__ ClearBatch C, uint64_t na,
                                                uint64_t nb) {
     uint64_t pol;
+#if LHC_CLEAR_POLICY == 0
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#elif LHC_CLEAR_POLICY == 1
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
     uint4* a = C.counters[blockIdx.y];
     uint32_t* b = C.bitmap[blockIdx.y];
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;

@@ -301,7 +301,7 @@ def main():
         # all local workers' gradients in one compress launch (sketch_compress_batch)
         dst = run.worker_sketches if run.per_worker else [run.sketch] * len(xs)
         clr = run.worker_sketches if run.per_worker else [run.sketch]
-        lhc.sketch_clear_batch(p, [t.bitmap for t in clr], [t.counters for t in clr])
+        lhc.sketch_clear_batch(p, [t.bitmap for t in clr[::-1]], [t.counters for t in clr[::-1]])
         cnt()
         mark("compress0")
         lhc.sketch_compress_batch(p, xs, [t.bitmap for t in dst], [t.counters for t in dst])
@@ -329,7 +329,7 @@ def main():
     def sharded_step(mark, cnt):
         targets = run.worker_bufs if run.per_worker else [run.slots] * len(xs)
         clr = [sk for bufs in (run.worker_bufs if run.per_worker else [run.slots]) for sk in bufs]
-        lhc.sketch_clear_batch(run.ps[0], [sk.bitmap for sk in clr], [sk.counters for sk in clr])
+        lhc.sketch_clear_batch(run.ps[0], [sk.bitmap for sk in clr[::-1]], [sk.counters for sk in clr[::-1]])
         cnt()
         mark("compress0")
         # every (worker, shard) pair in one launch

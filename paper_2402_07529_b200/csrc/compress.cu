@@ -112,13 +112,6 @@ __host__ __device__ constexpr size_t compress_warp_smem(uint32_t n_map) {
             ((n_map * 8 + 15) / 16) * 16 + kStages * sizeof(uint64_t) + 127) / 128 * 128;
 }
 
-// input of a global chunk index (the batch's chunk ranges are consecutive)
-__device__ __forceinline__ uint32_t batch_input(const CompressBatch& B, uint64_t g) {
-    uint32_t b = 0;
-    while (b + 1 < B.n && g >= B.start[b + 1]) b++;
-    return b;
-}
-
 __global__ void __launch_bounds__(kCompressThreads)
 k_compress_dense(KParams P, const __grid_constant__ CompressBatch B,
                  unsigned long long* __restrict__ nnz_out) {
@@ -146,25 +139,41 @@ k_compress_dense(KParams P, const __grid_constant__ CompressBatch B,
     __syncwarp();
     // prologue: the first kStages - 1 chunks in flight
     // whole chunks are bulk-copied; the ragged last chunk of an input is loaded plainly
-    auto prefetch = [&](uint64_t g, uint32_t sa) {
+    // the chunks a warp visits increase monotonically, so the input of the chunk being
+    // prefetched (pa) and of the chunk being processed (bi) only ever advance
+    uint32_t pa = 0;
+    uint64_t pa_start = 0, pa_next = B.n > 1 ? B.start[1] : nchunks, pa_full = B.d[0] / kTile;
+    const float* pa_x = B.x[0];
+    auto prefetch = [&](uint64_t g, uint32_t sa, bool fence) {
         if (g >= nchunks) return;
-        const uint32_t b = batch_input(B, g);
-        const uint64_t lc = g - B.start[b];
-        if (lc < (uint64_t)B.d[b] / kTile)
-            bulk_load(sh_x + sa * kTile, B.x[b] + lc * kTile, kTile * 4, bar + sa, pol_stream);
+        while (g >= pa_next) {
+            pa++;
+            pa_start = B.start[pa];
+            pa_next = pa + 1 < B.n ? B.start[pa + 1] : nchunks;
+            pa_full = B.d[pa] / kTile;
+            pa_x = B.x[pa];
+        }
+        const uint64_t lc = g - pa_start;
+        if (lc < pa_full) {
+            if (fence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(sh_x + sa * kTile, pa_x + lc * kTile, kTile * 4, bar + sa, pol_stream);
+        }
     };
     if (lane == 0)
-        for (int st = 0; st < kStages - 1; st++) prefetch(first + st * stride, st);
+        for (int st = 0; st < kStages - 1; st++) prefetch(first + st * stride, st, false);
+    uint32_t bi = 0;
+    uint64_t bi_start = 0, bi_next = B.n > 1 ? B.start[1] : nchunks;
     uint32_t it = 0, phase = 0;
     for (uint64_t chunk = first; chunk < nchunks; chunk += stride, it++) {
         const uint32_t st = it % kStages;
         // refill: the stage consumed in the previous iteration takes chunk + (kStages-1) stride
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            prefetch(chunk + (uint64_t)(kStages - 1) * stride, (it + kStages - 1) % kStages);
+        if (lane == 0) prefetch(chunk + (uint64_t)(kStages - 1) * stride, (it + kStages - 1) % kStages, true);
+        while (chunk >= bi_next) {
+            bi++;
+            bi_start = B.start[bi];
+            bi_next = bi + 1 < B.n ? B.start[bi + 1] : nchunks;
         }
-        const uint32_t bi = batch_input(B, chunk);
-        const uint64_t lchunk = chunk - B.start[bi];
+        const uint64_t lchunk = chunk - bi_start;
         const uint32_t d_in = B.d[bi];
         const float* __restrict__ x = B.x[bi];
         uint32_t* __restrict__ bitmap = B.bitmap[bi];

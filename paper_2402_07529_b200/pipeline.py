@@ -218,7 +218,8 @@ class LosslessAllReduce:
 
     def _step(self, items, stream):
         targets = self.worker_sketches if self.per_worker else [self.sketch]
-        L.sketch_clear_batch(self.p, [t.bitmap for t in targets], [t.counters for t in targets],
+        # cleared in reverse so the first sketches compressed are the last written (in L2)
+        L.sketch_clear_batch(self.p, [t.bitmap for t in targets[::-1]], [t.counters for t in targets[::-1]],
                              stream)
         if self.per_worker:
             dst = self.worker_sketches[:len(items)]
@@ -350,7 +351,7 @@ class ShardedAllReduce:
         targets = self.worker_bufs[:len(items)] if self.per_worker else [self.slots] * len(items)
         clear = self.worker_bufs if self.per_worker else [self.slots]
         flat = [sk for bufs in clear for sk in bufs]
-        L.sketch_clear_batch(self.ps[0], [sk.bitmap for sk in flat], [sk.counters for sk in flat],
+        L.sketch_clear_batch(self.ps[0], [sk.bitmap for sk in flat[::-1]], [sk.counters for sk in flat[::-1]],
                              stream)
         if coo:
             for bufs, item in zip(targets, items):

@@ -625,18 +625,25 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                              out_peeled, stats, n_c, sh_q, &sh_n, &sh_base, &sh_peeled);
 }
 
+constexpr uint64_t kSmallPeelCells = 1ull << 20;
+
 static size_t peel_smem(uint32_t k) { return (size_t)kPeelThreads * peel_q_per_thread(k) * sizeof(uint2); }
 
 template <int KT>
-static int peel_grid(int dev, uint32_t k) {
-    static int cached[64][kMaxK + 1] = {};
-    if (dev < 64 && cached[dev][k]) return cached[dev][k];
+static int peel_grid(int dev, uint32_t k, bool small) {
+    static int cached[64][kMaxK + 1][2] = {};
+    if (dev < 64 && cached[dev][k][small]) return cached[dev][k][small];
     const size_t smem = peel_smem(k);
     cudaFuncSetAttribute(k_peel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel<KT>, kPeelThreads, smem);
+    // small decode states (a shard's): the rounds are barrier-bound and a grid
+    // barrier over one CTA per SM is cheaper (NCF / 4: 162 vs 177 us)
+    if (small) per_sm = 1;
+    // experiment hook: fewer co-resident CTAs per SM
+    if (const char* ev = getenv("LHC_PEEL_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(ev)));
     int g = std::max(1, per_sm) * num_sms();
-    if (dev < 64) cached[dev][k] = g;
+    if (dev < 64) cached[dev][k][small] = g;
     return g;
 }
 
@@ -649,6 +656,7 @@ cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* ta
 #endif
     int dev = 0;
     cudaGetDevice(&dev);
+    const bool small = P.c <= kSmallPeelCells;
     KParams Pc = P;
     void* args[] = {(void*)&Pc,    (void*)&counters, (void*)&tabS,    (void*)&cand,
                     (void*)&dense, (void*)&cap,      (void*)&cells,   (void*)&claim,
@@ -656,10 +664,10 @@ cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* ta
                     (void*)&stats, (void*)&mode};
     cudaError_t err;
     if (P.k == 3)
-        err = cudaLaunchCooperativeKernel((const void*)k_peel<3>, dim3(peel_grid<3>(dev, 3)),
+        err = cudaLaunchCooperativeKernel((const void*)k_peel<3>, dim3(peel_grid<3>(dev, 3, small)),
                                           dim3(kPeelThreads), args, peel_smem(3), s);
     else
-        err = cudaLaunchCooperativeKernel((const void*)k_peel<0>, dim3(peel_grid<0>(dev, P.k)),
+        err = cudaLaunchCooperativeKernel((const void*)k_peel<0>, dim3(peel_grid<0>(dev, P.k, small)),
                                           dim3(kPeelThreads), args, peel_smem(P.k), s);
     count_launch();
     return err;

@@ -515,8 +515,18 @@ def main():
         coo_host = [wl.coo(w) for w in my_workers]
         if sharded:   # per-shard lists with shard-relative indices (split once on the host)
             coo_host = [c for i, v in coo_host for c in run.split_coo(i, v)]
-        pin_i = [torch.from_numpy(i.view(np.int32)).pin_memory() for i, _ in coo_host]
-        pin_v = [torch.from_numpy(v).pin_memory() for _, v in coo_host]
+        # all lists packed into one pinned host buffer (one H2D copy per step): for
+        # list j, indices at [off_j, off_j + n_j), values at [tot + off_j, ...)
+        lens = [len(i) for i, _ in coo_host]
+        offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        tot = int(offs[-1])
+        pin_all = torch.empty(2 * tot, dtype=torch.int32).pin_memory()
+        pa = pin_all.numpy()
+        for j, (i, v) in enumerate(coo_host):
+            pa[offs[j]:offs[j + 1]] = i.view(np.int32)
+            pa[tot + offs[j]:tot + offs[j + 1]] = v.view(np.int32)
+        pin_i = [pin_all[offs[j]:offs[j + 1]] for j in range(len(lens))]
+        pin_v = [pin_all[tot + offs[j]:tot + offs[j + 1]].view(torch.float32) for j in range(len(lens))]
         if sharded:
             run_b = lhc.ShardedAllReduce(run.plan, seed=SEED, local_workers=len(xs),
                                          per_worker=not args.fuse_local, device=dev, comm=args.comm)
@@ -529,11 +539,14 @@ def main():
             run_b = lhc.LosslessAllReduce(p, cap, local_workers=len(xs),
                                           per_worker=not args.fuse_local, comm=comm_b, device=dev)
         engines = [run, run_b]
-        ins, items_k, outs = [], [], []
+        ins, items_k, outs, dev_alls = [], [], [], []
         cap_ = run.decoder.cap
         for k in range(2):
-            dev_i = [torch.empty_like(t, device=dev) for t in pin_i]
-            dev_v = [torch.empty_like(t, device=dev) for t in pin_v]
+            dev_all = torch.empty(2 * tot, dtype=torch.int32, device=dev)
+            dev_i = [dev_all[offs[j]:offs[j + 1]] for j in range(len(lens))]
+            dev_v = [dev_all[tot + offs[j]:tot + offs[j + 1]].view(torch.float32)
+                     for j in range(len(lens))]
+            dev_alls.append(dev_all)
             ins.append((dev_i, dev_v))
             pairs = list(zip(dev_i, dev_v))
             items_k.append([pairs[w * G:(w + 1) * G] for w in range(len(my_workers))]
@@ -552,8 +565,7 @@ def main():
             k = i % 2
             s_in.wait_event(ev["comp"][k])            # step i-2 no longer reads ins[k]
             with torch.cuda.stream(s_in):
-                for a, b_ in zip(pin_i + pin_v, ins[k][0] + ins[k][1]):
-                    b_.copy_(a, non_blocking=True)
+                dev_alls[k].copy_(pin_all, non_blocking=True)
                 ev["in"][k].record(s_in)
             s_comp.wait_event(ev["in"][k])
             s_comp.wait_event(ev["out"][k])           # step i-2's results have left

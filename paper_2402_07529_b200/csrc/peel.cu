@@ -640,8 +640,6 @@ static int peel_grid(int dev, uint32_t k, bool small) {
     // small decode states (a shard's): the rounds are barrier-bound and a grid
     // barrier over one CTA per SM is cheaper (NCF / 4: 162 vs 177 us)
     if (small) per_sm = 1;
-    // experiment hook: fewer co-resident CTAs per SM
-    if (const char* ev = getenv("LHC_PEEL_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(ev)));
     int g = std::max(1, per_sm) * num_sms();
     if (dev < 64) cached[dev][k][small] = g;
     return g;

@@ -18,6 +18,9 @@ __global__ void k(void* buf, uint32_t mask, uint32_t iters, unsigned long long* 
         if (OP == 1) acc += atomicAdd(reinterpret_cast<unsigned long long*>(buf) + i, 1ull);  // ATOM u64
         if (OP == 2) acc += atomicCAS(reinterpret_cast<uint32_t*>(buf) + 2 * i, 0xffffffffu, 1u);
         if (OP == 3) acc += __ldcg(reinterpret_cast<unsigned long long*>(buf) + i);   // plain random load
+        if (OP == 4) atomicAdd(reinterpret_cast<unsigned long long*>(buf) + i, 1ull);  // RED u64
+        if (OP == 5) atomicAdd(reinterpret_cast<uint32_t*>(buf) + 2 * i, 1u);           // RED u32
+        if (OP == 6) acc += atomicAdd(reinterpret_cast<uint32_t*>(buf) + 2 * i, 1u);    // ATOM u32
     }
     if (acc == 0x123456789ull) *sink = acc;
 }
@@ -25,10 +28,11 @@ int main() {
     void* buf; unsigned long long* sink;
     cudaMalloc(&buf, 1ull << 31); cudaMalloc(&sink, 8); cudaMemset(buf, 0, 1ull << 31);
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const char* names[] = {"RED.F32", "ATOM.ADD.U64(ret)", "ATOM.CAS.B32(ret)", "LDG.64 random"};
+    const char* names[] = {"RED.F32", "ATOM.ADD.U64(ret)", "ATOM.CAS.B32(ret)", "LDG.64 random",
+                           "RED.ADD.U64", "RED.ADD.U32", "ATOM.ADD.U32(ret)"};
     for (uint32_t logb : {26u, 31u}) {  // 64 MB (L2-resident) and 2 GB (HBM)
         uint32_t mask = (uint32_t)((1ull << logb) / 8 - 1);
-        for (int op = 0; op < 4; op++) {
+        for (int op = 0; op < 7; op++) {
             int blocks = sms * 8, threads = 256; uint32_t iters = 64;
             cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
             for (int rep = 0; rep < 2; rep++) {
@@ -37,6 +41,9 @@ int main() {
                 if (op == 1) k<1><<<blocks, threads>>>(buf, mask, iters, sink);
                 if (op == 2) k<2><<<blocks, threads>>>(buf, mask, iters, sink);
                 if (op == 3) k<3><<<blocks, threads>>>(buf, mask, iters, sink);
+                if (op == 4) k<4><<<blocks, threads>>>(buf, mask, iters, sink);
+                if (op == 5) k<5><<<blocks, threads>>>(buf, mask, iters, sink);
+                if (op == 6) k<6><<<blocks, threads>>>(buf, mask, iters, sink);
                 cudaEventRecord(b); cudaEventSynchronize(b);
             }
             float ms; cudaEventElapsedTime(&ms, a, b);

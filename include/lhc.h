@@ -61,6 +61,10 @@ typedef struct lhc_params {
                         * LHC_INDEX_BITMAP: the exact bitmap index of §3.2 (one bit *
                         * per parameter, bit p = coordinate p; requires m = ceil(d/L)*L)    */
     uint32_t L;        /* batch width, power of two in [32, 1024] (paper: c=1024)  */
+    uint32_t blocks;   /* 0: one Count Sketch over all rows; B > 0: the sketch is split into
+                          B blocks of k partitions ("splitting the Count Sketch into
+                          multiple blocks of fixed size"): input row i hashes only into
+                          block i mod B (c must be a multiple of B*k*L)                    */
     uint64_t seed;     /* hash seed; every rank must use the same one                       */
 } lhc_params;
 

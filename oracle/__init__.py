@@ -41,6 +41,7 @@ class Params(ctypes.Structure):
         ("k", ctypes.c_uint32),
         ("k_bloom", ctypes.c_uint32),
         ("L", ctypes.c_uint32),
+        ("blocks", ctypes.c_uint32),
         ("seed", ctypes.c_uint64),
     ]
 
@@ -109,8 +110,9 @@ def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
 
-def params(d, m, c, k=3, k_bloom=0, L=1024, seed=0) -> Params:
-    return Params(int(d), int(m), int(c), int(k), int(k_bloom), int(L), int(seed) & (2**64 - 1))
+def params(d, m, c, k=3, k_bloom=0, L=1024, seed=0, blocks=0) -> Params:
+    return Params(int(d), int(m), int(c), int(k), int(k_bloom), int(L), int(blocks),
+                  int(seed) & (2**64 - 1))
 
 
 INDEX_BITMAP = 255  # k_bloom value of the exact bitmap index

@@ -54,6 +54,7 @@ typedef struct {
     uint32_t k;        /* Count Sketch hashes (paper: 3)                */
     uint32_t k_bloom;  /* Bloom probes (paper: log 1/eps); 0 means k    */
     uint32_t L;        /* batch width (paper: c = 1024)                 */
+    uint32_t blocks;   /* 0, or the Count Sketch split into blocks     */
     uint64_t seed;     /* hash seed                                             */
 } ora_params;
 
@@ -116,10 +117,18 @@ void ora_row_map(const ora_params* p, uint32_t dom, uint32_t j, uint64_t i,
         *sign = +1;
         return;
     }
+    /* blocked Count Sketch ("splitting the Count Sketch into multiple blocks
+     * of fixed size", reading R25): input row i belongs to block i mod blocks, whose
+     * k partitions of S rows each hold all of its cells */
+    uint64_t base = 0;
     uint64_t S = dom == 0 ? p->c / ((uint64_t)p->k * p->L)
                           : p->m / ((uint64_t)kb_of(p) * p->L);
+    if (dom == 0 && p->blocks) {
+        S = p->c / ((uint64_t)p->blocks * p->k * p->L);
+        base = (i % p->blocks) * p->k * S;
+    }
     uint64_t H = ora_hash(p->seed, dom, j, i);
-    *row = (uint64_t)j * S + (((H >> 32) * S) >> 32);
+    *row = base + (uint64_t)j * S + (((H >> 32) * S) >> 32);
     *bias = (uint32_t)(H & (uint64_t)(p->L - 1));
     *sign = ((H >> 16) & 1) ? -1 : +1;
 }
@@ -163,6 +172,7 @@ int ora_validate(const ora_params* p)
     if (p->m == 0 || p->m % ((uint64_t)kb * p->L)) return ORA_EINVAL;
     if (p->c / ((uint64_t)p->k * p->L) >= (1ull << 32)) return ORA_EINVAL;
     if (p->m / ((uint64_t)kb * p->L) >= (1ull << 32)) return ORA_EINVAL;
+    if (p->blocks && p->c % ((uint64_t)p->blocks * p->k * p->L)) return ORA_EINVAL;
     return ORA_OK;
 }
 

@@ -37,12 +37,13 @@ class lhc_params(ctypes.Structure):
         ("k", ctypes.c_uint32),
         ("k_bloom", ctypes.c_uint32),
         ("L", ctypes.c_uint32),
+        ("blocks", ctypes.c_uint32),
         ("seed", ctypes.c_uint64),
     ]
 
     def __repr__(self):
         return (f"lhc_params(d={self.d}, m={self.m}, c={self.c}, k={self.k}, "
-                f"k_bloom={self.k_bloom}, L={self.L}, seed={self.seed:#x})")
+                f"k_bloom={self.k_bloom}, L={self.L}, blocks={self.blocks}, seed={self.seed:#x})")
 
     @property
     def kb(self) -> int:
@@ -171,8 +172,8 @@ def _dev(t: torch.Tensor | None, dtype, numel: int | None, name: str) -> int | N
     return t.data_ptr()
 
 
-def params(d, m, c, k=3, k_bloom=0, L=1024, seed=0) -> lhc_params:
-    return lhc_params(int(d), int(m), int(c), int(k), int(k_bloom), int(L),
+def params(d, m, c, k=3, k_bloom=0, L=1024, seed=0, blocks=0) -> lhc_params:
+    return lhc_params(int(d), int(m), int(c), int(k), int(k_bloom), int(L), int(blocks),
                       int(seed) & (2**64 - 1))
 
 

@@ -77,6 +77,8 @@ int validate(const lhc_params* p) {
     if (p->m == 0 || p->m % ((uint64_t)kb * p->L)) return set_error(LHC_EINVAL, "m must be a positive multiple of k_bloom*L");
     if (p->c >= (1ull << 32)) return set_error(LHC_EINVAL, "c must be < 2^32");
     if (p->m / p->L >= (1ull << 32)) return set_error(LHC_EINVAL, "m/L must be < 2^32");
+    if (p->blocks && p->c % ((uint64_t)p->blocks * p->k * p->L))
+        return set_error(LHC_EINVAL, "c must be a multiple of blocks*k*L");
     return LHC_OK;
 }
 
@@ -93,7 +95,9 @@ KParams kparams(const lhc_params* p) {
     K.log2L = ilog2(p->L);
     K.nw = p->L / 32;
     K.log2nw = ilog2(K.nw);
-    K.S_Y = (uint32_t)(p->c / ((uint64_t)K.k * p->L));
+    K.blocks = p->blocks;
+    // rows per Count Sketch partition (per block when the sketch is blocked)
+    K.S_Y = (uint32_t)(p->c / ((uint64_t)(p->blocks ? p->blocks : 1) * K.k * p->L));
     K.S_B = (uint32_t)(p->m / ((uint64_t)K.kb * p->L));
     K.nrows = (uint32_t)(((uint64_t)p->d + p->L - 1) / p->L);
     return K;

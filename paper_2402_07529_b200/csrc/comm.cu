@@ -759,6 +759,15 @@ __device__ void nv_barrier(cg::grid_group& grid, const NvArgs& A, uint32_t targe
     grid.sync();
 }
 
+#ifndef LHC_NV_TIMING
+#define LHC_NV_TIMING 0
+#endif
+// debug: block 0 stamps phase boundaries into the signal area (u64 slots from byte 512)
+__device__ __forceinline__ void nv_stamp(const NvArgs& A, int k) {
+    if (LHC_NV_TIMING && blockIdx.x == 0 && threadIdx.x == 0)
+        reinterpret_cast<unsigned long long*>(A.sig_uc + 128)[k] = globaltimer();
+}
+
 // 16-byte unit u of the multicast view: OR (bitmap) or sum (counters) over ranks
 __device__ __forceinline__ float4 nv_reduce_unit(const NvArgs& A, uint64_t off_bytes, bool is_or) {
     if (is_or) {
@@ -780,7 +789,9 @@ __global__ void __launch_bounds__(256) k_allreduce_nvls(NvArgs A) {
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
     const uint32_t epoch = *(volatile uint32_t*)(A.sig_uc + 16);
+    nv_stamp(A, 0);
     nv_barrier(grid, A, (epoch + 1) * (uint32_t)A.world);  // every rank's sketch is complete
+    nv_stamp(A, 1);
     // kNvU switch reductions in flight per thread
     for (uint64_t u0 = A.lo + gtid; u0 < A.hi; u0 += kNvU * gstride) {
         float4 v[kNvU];
@@ -795,7 +806,9 @@ __global__ void __launch_bounds__(256) k_allreduce_nvls(NvArgs A) {
             if (u < A.hi) mm_st_v4(reinterpret_cast<float*>(A.mc + u * 16), v[a]);
         }
     }
+    nv_stamp(A, 2);
     nv_barrier(grid, A, (epoch + 2) * (uint32_t)A.world);  // every slice is everywhere
+    nv_stamp(A, 3);
     if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile uint32_t*)(A.sig_uc + 16) = epoch + 2;
 }
 

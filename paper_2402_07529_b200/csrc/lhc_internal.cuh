@@ -26,6 +26,7 @@ struct KParams {
     uint32_t S_B;      // rows per bloom partition
     uint32_t nrows;    // ceil(d / L)
     uint32_t exact;    // 1: the index is the exact bitmap, bit p <-> coordinate p
+    uint32_t blocks;   // 0, or Count Sketch blocks: row i -> block i mod blocks
 };
 
 // ---------------------------------------------------------------------------
@@ -61,7 +62,9 @@ __host__ __device__ __forceinline__ uint2 row_map(uint64_t seed, uint32_t dom, u
 __host__ __device__ __forceinline__ uint2 dom_map(const KParams& P, uint32_t dom, uint32_t j,
                                                   uint64_t i) {
     if (dom == 1 && P.exact) return make_uint2((uint32_t)i, 0u);
-    return row_map(P.seed, dom, j, i, dom ? P.S_B : P.S_Y, P.L);
+    uint2 mp = row_map(P.seed, dom, j, i, dom ? P.S_B : P.S_Y, P.L);
+    if (dom == 0 && P.blocks) mp.x += (uint32_t)(i % P.blocks) * P.k * P.S_Y;  // block base
+    return mp;
 }
 
 __device__ __forceinline__ uint32_t map_bias(uint2 mp) { return mp.y & 0x7fffffffu; }

@@ -215,7 +215,7 @@ k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __rest
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t D = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); D < nD;
          D += warps) {
-        const uint32_t j = (uint32_t)(D / P.S_Y);
+        const uint32_t j = (uint32_t)((D % ((uint64_t)P.k * P.S_Y)) / P.S_Y);  // probe of row D
         Acc acc[32];
 #pragma unroll
         for (int c = 0; c < 32; c++) acc[c] = 0;
@@ -366,7 +366,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
             for (int u = 0; u < 4; u++)
                 if (C::deg(key[u]) == 1u) {
                     const uint32_t e = (uint32_t)(base + u * gstride + threadIdx.x);
-                    const uint32_t id = COMPACT ? C::low(key[u]) | (((e >> P.log2L) / P.S_Y) << 24)
+                    const uint32_t id = COMPACT ? C::low(key[u]) | ((((e >> P.log2L) % (P.k * P.S_Y)) / P.S_Y) << 24)
                                                 : C::low(key[u]);
                     sh_q[atomicAdd(sh_n, 1u)] = make_uint2(e, id);
                 }

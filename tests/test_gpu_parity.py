@@ -40,7 +40,7 @@ def gpu_params(lhc, d, m, c, k=3, kb=0, L=1024, seed=0):
 
 
 def ora_params(ora, p):
-    return ora.params(p.d, p.m, p.c, p.k, p.k_bloom, p.L, p.seed)
+    return ora.params(p.d, p.m, p.c, p.k, p.k_bloom, p.L, p.seed, p.blocks)
 
 
 def make_workers(d, nnz, W, seed, law="dyadic", structure="uniform", run=64, sigma=1e-3):
@@ -492,3 +492,35 @@ def test_paper_optimal_bloom_pipeline(lhc, ora, density):
     assert np.array_equal(U(run.sketch.bitmap), B)
     st = compare_decode(ora, dec, ref, True)
     assert st["success"]
+
+
+# ------------------------------------------ NEXT-3: blocked Count Sketch (R25) --
+
+def blocked_params(lhc, d, nnz, W, L, B, gamma=1.5, seed=0xB10C):
+    s = lhc.size_workload(d, nnz / d, W, L=L)
+    S = max(1, int(np.ceil(gamma * s.n_cand_expected / (B * 3 * L))))
+    return lhc.params(d, s.m, B * 3 * S * L, 3, 0, L, seed + B, B)
+
+
+@pytest.mark.parametrize("d,nnz,W,L,B", [
+    (1_000_003, 10_000, 3, 128, 64),      # ragged tail, many blocks
+    (300_000, 6_000, 2, 1024, 8),
+    (777_777, 30_000, 4, 256, 33),         # B does not divide the row count
+])
+@pytest.mark.parametrize("law", ["dyadic", "gauss"])
+@pytest.mark.parametrize("build", ["insert", "rows", "compact"])
+def test_blocked_sketch_pipeline(lhc, ora, d, nnz, W, L, B, law, build, monkeypatch):
+    """P:L206 blocks: every row map, the bitmap, counters, candidates, flags, rounds
+    and values equal the oracle's on a blocked sketch, through every build mode of
+    the peeling state."""
+    monkeypatch.setenv("LHC_CELL_BUILD", build)
+    p = blocked_params(lhc, d, nnz, W, L, B)
+    op = ora_params(ora, p)
+    xs = make_workers(d, nnz, W, 50 + B, law)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B_, Y, ref = ora.pipeline(op, xs)
+    assert np.array_equal(U(run.sketch.bitmap), B_)
+    assert_values(F(run.sketch.counters), Y, law == "dyadic")
+    compare_decode(ora, dec, ref, law == "dyadic")

@@ -504,3 +504,53 @@ def test_exact_bitmap_lossless(ora):
     truth = np.sum(np.stack(xs).astype(np.float64), axis=0)
     assert dec.stats.success and np.array_equal(dec.dense, truth)
     assert dec.stats.n_cand == int((np.stack(xs) != 0).any(axis=0).sum())  # no false positives
+
+
+# ------------------------------------------ NEXT-3: blocked Count Sketch (R25) --
+
+def test_one_block_is_the_unblocked_sketch(ora):
+    # P:L206 blocks: with a single block every map must equal the unblocked one
+    d, L = 50 * 1024, 1024
+    a = ora.params(d, 3 * L * 8, 3 * L * 20, 3, 0, L, 99, 0)
+    b = ora.params(d, 3 * L * 8, 3 * L * 20, 3, 0, L, 99, 1)
+    for q in range(0, d, 997):
+        for j in range(3):
+            assert ora.cell(a, j, q) == ora.cell(b, j, q)
+            assert ora.bit(a, j, q) == ora.bit(b, j, q)   # the index is not blocked
+
+
+def test_blocked_cells_stay_in_their_block(ora):
+    # every coordinate of input row i lands in block i mod B, probe j in the j-th
+    # partition of that block (S rows each), and the blocks are used evenly
+    d, L, B, S = 97 * 256, 256, 7, 5
+    c = B * 3 * S * L
+    p = ora.params(d, 3 * L * 4, c, 3, 0, L, 7, B)
+    used = np.zeros(c // L, np.int64)
+    for q in range(0, d, 13):
+        i = q // L
+        for j in range(3):
+            row = ora.cell(p, j, q)[0] // L
+            lo = (i % B) * 3 * S + j * S
+            assert lo <= row < lo + S, (q, j, row, lo)
+            used[row] += 1
+    per_block = used.reshape(B, 3 * S).sum(axis=1)
+    assert per_block.min() > 0.8 * per_block.mean()
+
+
+@pytest.mark.parametrize("B", [4, 16])
+def test_blocked_sketch_is_lossless(ora, B):
+    # the method stays exact with a blocked sketch at gamma_s = 1.5
+    d, L, W, nnz = 64 * 128, 128, 3, 300
+    n = d * (1 - (1 - nnz / d) ** W)
+    S = max(1, math.ceil(1.5 * n / (B * 3 * L)))
+    c = B * 3 * S * L
+    p = ora.params(d, 3 * L * 64, c, 3, 0, L, 1234 + B, B)
+    rng = rng_for(3100 + B)
+    xs = []
+    for w in range(W):
+        x = np.zeros(d, np.float32)
+        x[support(rng, d, nnz)] = values(rng, nnz, "dyadic")
+        xs.append(x)
+    _, _, ref = ora.pipeline(p, xs)
+    assert ref.stats.success
+    assert np.array_equal(ref.dense, np.sum(np.stack(xs).astype(np.float64), axis=0))

@@ -119,6 +119,7 @@ WsLayout ws_layout(const KParams& P, uint64_t cap) {
     W.dst_off = o;   o = align_up(o + ((P.c >> P.log2L) + 1) * sizeof(uint32_t), 256);
     W.pair_pos = o;  o = align_up(o + (size_t)P.nrows * P.k * sizeof(uint32_t), 256);
     W.dst_list = o;  o = align_up(o + (size_t)P.nrows * P.k * sizeof(uint32_t), 256);
+    W.rowoff = o;    o = align_up(o + ((size_t)P.nrows + 1) * sizeof(uint32_t), 256);
     W.total = o;
     return W;
 }
@@ -262,6 +263,7 @@ struct WsView {
     uint2* frontier;
     float* dense;
     uint32_t *dst_off, *pair_pos, *dst_list;
+    uint32_t* rowoff;
 };
 
 int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, WsView* v) {
@@ -274,6 +276,7 @@ int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, 
     if (ws_bytes < v->W.total)
         return set_error(LHC_ECAPACITY, "workspace too small: %zu < %zu bytes", ws_bytes, v->W.total);
     char* b = static_cast<char*>(ws);
+    v->rowoff = reinterpret_cast<uint32_t*>(b + v->W.rowoff);
     v->ctrl = reinterpret_cast<Ctrl*>(b + v->W.ctrl);
     v->tabS = reinterpret_cast<uint2*>(b + v->W.tabS);
     v->gmask = reinterpret_cast<uint32_t*>(b + v->W.gmask);
@@ -301,7 +304,7 @@ int sketch_query(const lhc_params* p, const uint32_t* bitmap, void* ws, size_t w
     if (cudaMemsetAsync(v.ctrl, 0, sizeof(Ctrl), s) != cudaSuccess) return check_launch("memset");
     if (cudaMemsetAsync(stats, 0, sizeof(lhc_stats), s) != cudaSuccess) return check_launch("memset");
     cudaError_t e = launch_query(v.P, bitmap, v.tabS, v.gmask, v.cta_total, cap_cand, out_idx,
-                                 v.ctrl, stats, s);
+                                 v.ctrl, stats, v.rowoff, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "query launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_query");
 }
@@ -322,14 +325,23 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
     // HBM reductions), compact (8 B/cell) when the input rows fit in 22 bits;
     // otherwise the in-kernel per-candidate insert is faster.
     // (LHC_CELL_BUILD=rows|compact|insert overrides the choice; results are identical)
+    // A blocked sketch is peeled block by block in shared memory; the global
+    // peel then runs only if a block could not be (mode 3: fallback, device-checked).
     int mode = p->c * sizeof(CellState) > (size_t)l2_bytes() / 2 ? 1 : 0;
     if (mode == 1 && v.P.nrows <= (1u << 22)) mode = 2;
+    bool blocked = peel_blocked_fits(v.P);
     if (const char* ev = getenv("LHC_CELL_BUILD")) {
-        if (!strcmp(ev, "rows")) mode = 1;
-        if (!strcmp(ev, "compact")) mode = v.P.nrows <= (1u << 22) ? 2 : 1;
-        if (!strcmp(ev, "insert")) mode = 0;
+        if (!strcmp(ev, "rows")) mode = 1, blocked = false;
+        if (!strcmp(ev, "compact")) mode = v.P.nrows <= (1u << 22) ? 2 : 1, blocked = false;
+        if (!strcmp(ev, "insert")) mode = 0, blocked = false;
     }
-    if (mode)
+    if (blocked) {
+        cudaError_t eb = launch_peel_blocked(v.P, counters, v.tabS, v.gmask, v.rowoff, dense, cap_cand,
+                                             out_val, out_peeled, v.ctrl, stats, s);
+        if (eb != cudaSuccess) return set_error(LHC_ECUDA, "blocked peel launch: %s", cudaGetErrorString(eb));
+        mode = 3;
+    }
+    if (mode == 1 || mode == 2)
         launch_build_cells(v.P, counters, v.tabS, v.gmask, v.dst_off, v.pair_pos, v.dst_list,
                            v.cells, v.ctrl, mode == 2, s);
     cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, dense, cap_cand, v.cells, v.claim,

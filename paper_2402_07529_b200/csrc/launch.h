@@ -41,7 +41,13 @@ void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* co
 constexpr uint32_t kMaxQueryCtas = 4096;
 cudaError_t launch_query(const KParams& P, const uint32_t* bitmap, uint2* tabS, uint32_t* gmask,
                          uint32_t* cta_total, uint64_t cap, uint32_t* out_idx, Ctrl* ctrl,
-                         lhc_stats* stats, cudaStream_t s);
+                         lhc_stats* stats, uint32_t* rowoff, cudaStream_t s);
+// block-local peel of a blocked sketch (peel.cu); false if a block does not fit
+bool peel_blocked_fits(const KParams& P);
+cudaError_t launch_peel_blocked(const KParams& P, const float* counters, const uint2* tabS,
+                                const uint32_t* gmask, const uint32_t* rowoff, float* dense,
+                                uint64_t cap, float* out_val, uint8_t* out_peeled, Ctrl* ctrl,
+                                lhc_stats* stats, cudaStream_t s);
 uint32_t query_max_ctas();
 
 // peeling decoder (peel.cu)

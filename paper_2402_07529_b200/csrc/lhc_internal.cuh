@@ -106,6 +106,10 @@ struct Ctrl {
     unsigned long long rc[3];
     uint32_t rounds_dbg;
     uint32_t compact_fail;  // set by k_build_cells<compact> when a row is too full
+    uint32_t blk_fail;      // set by k_peel_blocked when a block cannot be peeled in place
+    uint32_t blk_done;      // blocks finished (the last one writes the stats)
+    unsigned long long blk_peeled;
+    uint32_t blk_rounds;
     // instrumentation (device globaltimer ns): t[0..3] phase starts, t[3 + r] start of
     // round r, t[kCtrlTimes-1] end of rounds; fsize[r] = queue segment of round r
     unsigned long long t[128];
@@ -123,7 +127,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // Sub-allocation of the decompress workspace.
 struct WsLayout {
-    size_t tabS, gmask, cta_total, cells, claim, frontier, dense, dst_off, pair_pos, dst_list, ctrl, total;
+    size_t tabS, gmask, cta_total, cells, claim, frontier, dense, dst_off, pair_pos, dst_list, ctrl,
+        rowoff, total;
     uint32_t nchunks;
 };
 

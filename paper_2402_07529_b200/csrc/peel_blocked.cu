@@ -1,0 +1,272 @@
+// peel_blocked.cu — Phase II steps 2-3 for a blocked Count Sketch
+// ("O(1) iterations by splitting the Count Sketch into multiple blocks of
+// fixed size"; reading R25): input row i hashes only into block i mod B, so the
+// peeling of different blocks is independent.  One CTA peels one block entirely
+// in shared memory:
+//   load   the block's counters (R), the query masks of its input rows and their
+//          first candidate slots (from the query), and zero its dense ranges
+//   insert every candidate p of the block adds (2^24 + local id) to the 32-bit key
+//          of each of its k cells (shared-memory atomics; the degree is key >> 24,
+//          exact whenever it is 0 or 1; the per-destination-row row counts are
+//          checked first so the degree cannot overflow 8 bits)
+//   rounds synchronous (reading R10): every thread scans its cells for degree 1
+//          into a register bitmask, __syncthreads, then peels them — claim bit
+//          (first claimer wins), val = sign * R, subtract from the other cells —
+//          __syncthreads; the rounds end when no cell of the block is pure
+//   final  median over j of sign_j * R for the candidates peeling did not reach
+//          (P:L155); values land in out_val / out_peeled at their slots and in the
+//          dense output at their coordinates
+// Block rounds are max-combined, so `rounds` equals the synchronous rounds of the
+// whole (block-diagonal) incidence, as in the oracle.  A block whose destination
+// rows collect more than kBlkMaxRows input rows sets ctrl->blk_fail and the global peel
+// (k_peel, launched after in fallback mode) decodes the sketch instead.
+#include "launch.h"
+
+namespace lhc {
+
+constexpr int kBlkThreads = 1024;
+constexpr int kBlkCellsPerThread = 32;  // a thread's pure-cell bitmask is one word
+// key = sum (2^24 + local id): with local ids < 2^24 and at most 127 input rows per
+// destination row (so degree <= 127), degree + carry of the id sum stays < 256 and
+// equals 1 only when the true degree is 1
+constexpr uint32_t kBlkMaxRows = 127;
+
+struct BlkArgs {
+    KParams P;
+    const float* counters;
+    const uint2* tabS;
+    const uint32_t* gmask;
+    const uint32_t* rowoff;
+    float* dense;
+    uint64_t cap;
+    float* out_val;
+    uint8_t* out_peeled;
+    Ctrl* ctrl;
+    lhc_stats* stats;
+    uint32_t rpb;  // input rows per block (upper bound)
+};
+
+// shared-memory layout of one block (32-bit words)
+__host__ __device__ inline size_t blk_smem_words(const KParams& P, uint32_t rpb) {
+    const size_t cb = (size_t)P.k * P.S_Y * P.L;           // cells of a block
+    return 2 * cb                                          // key, R
+           + 2 * (size_t)rpb * P.nw                        // masks, claim bits
+           + rpb                                           // first slots
+           + (size_t)P.k * P.S_Y;                          // input rows per destination row
+}
+
+__global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_constant__ BlkArgs A) {
+    extern __shared__ uint32_t sm[];
+    const KParams& P = A.P;
+    const uint32_t k = P.k, L = P.L, nw = P.nw;
+    const uint32_t SL = P.S_Y * L;                         // cells per partition of a block
+    const uint32_t cb = k * SL;
+    uint32_t* key = sm;
+    float* R = reinterpret_cast<float*>(sm + cb);
+    uint32_t* mask = sm + 2 * cb;
+    uint32_t* claim = mask + (size_t)A.rpb * nw;
+    uint32_t* first = claim + (size_t)A.rpb * nw;
+    uint32_t* rows_per_dst = first + A.rpb;
+    __shared__ uint32_t sh_peeled, sh_rounds, sh_fail;
+    const uint64_t n_c = *(volatile unsigned long long*)&A.ctrl->n_cand;
+    if (n_c > A.cap) return;  // overflow: the stats were set by the query
+
+    for (uint32_t b = blockIdx.x; b < P.blocks; b += gridDim.x) {
+        __syncthreads();  // the previous block's readers of the shared flags are done
+        const uint32_t nrb = b < P.nrows ? (P.nrows - 1 - b) / P.blocks + 1 : 0;  // rows of block b
+        const uint64_t cbase = (uint64_t)b * cb;           // first cell of the block
+        const uint32_t rbase = b * k * P.S_Y;              // first destination row
+        if (threadIdx.x == 0) { sh_peeled = 0; sh_rounds = 0; sh_fail = 0; }
+        // ---- load
+        for (uint32_t e = threadIdx.x; e < cb; e += blockDim.x) {
+            key[e] = 0u;
+            R[e] = __ldcs(A.counters + cbase + e);
+        }
+        for (uint32_t a = threadIdx.x; a < k * P.S_Y; a += blockDim.x) rows_per_dst[a] = 0u;
+        for (uint32_t a = threadIdx.x; a < nrb * nw; a += blockDim.x) {
+            const uint32_t t = a / nw, w = a - t * nw;
+            const uint64_t i = b + (uint64_t)t * P.blocks;
+            mask[a] = __ldcg(A.gmask + i * nw + w);
+            claim[a] = 0u;
+        }
+        for (uint32_t t = threadIdx.x; t < nrb; t += blockDim.x)
+            first[t] = __ldcg(A.rowoff + b + (uint64_t)t * P.blocks);
+        // the block's dense ranges are zeroed (values land there later)
+        for (uint32_t a = threadIdx.x; a < nrb * (L / 4); a += blockDim.x) {
+            const uint32_t t = a / (L / 4), u = a - t * (L / 4);
+            const uint64_t q0 = ((uint64_t)b + (uint64_t)t * P.blocks) * L + 4 * u;
+            if (q0 + 4 <= P.d) __stcs(reinterpret_cast<float4*>(A.dense + q0), make_float4(0.f, 0.f, 0.f, 0.f));
+            else for (uint64_t q = q0; q < P.d; q++) A.dense[q] = 0.f;
+        }
+        __syncthreads();
+        // ---- degree bound: input rows per destination row of the block
+        for (uint32_t a = threadIdx.x; a < nrb * k; a += blockDim.x) {
+            const uint32_t t = a / k, j = a - t * k;
+            const uint64_t i = b + (uint64_t)t * P.blocks;
+            atomicAdd(&rows_per_dst[__ldg(&A.tabS[i * k + j].x) - rbase], 1u);
+        }
+        __syncthreads();
+        for (uint32_t a = threadIdx.x; a < k * P.S_Y; a += blockDim.x)
+            if (rows_per_dst[a] > kBlkMaxRows) sh_fail = 1u;
+        __syncthreads();
+        if (sh_fail) {
+            if (threadIdx.x == 0) atomicOr(&A.ctrl->blk_fail, 1u);
+            continue;  // uniform
+        }
+        // ---- insert: (row t, word w) pairs, every set bit a candidate
+        for (uint32_t a = threadIdx.x; a < nrb * nw; a += blockDim.x) {
+            const uint32_t t = a / nw, w = a - t * nw;
+            uint32_t mm = mask[a];
+            if (!mm) continue;
+            const uint64_t i = b + (uint64_t)t * P.blocks;
+            for (uint32_t j = 0; j < k; j++) {
+                const uint2 mp = __ldg(&A.tabS[i * k + j]);
+                const uint32_t rowl = (mp.x - rbase) * L, bias = map_bias(mp);
+                for (uint32_t m2 = mm; m2; m2 &= m2 - 1) {
+                    const uint32_t col = 32 * w + (__ffs(m2) - 1);
+                    atomicAdd(&key[rowl + ((col + bias) & (L - 1))], (1u << 24) + t * L + col);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- synchronous rounds
+        for (;;) {
+            // A: pure cells at the start of the round (thread-strided, <= 32 per thread)
+            uint32_t pure = 0u;
+            for (uint32_t s = 0; s < kBlkCellsPerThread; s++) {
+                const uint32_t e = threadIdx.x + s * blockDim.x;
+                if (e < cb && (key[e] >> 24) == 1u) pure |= 1u << s;
+            }
+            if (!__syncthreads_or(pure != 0u)) break;
+            // B: peel them
+            uint32_t my_peeled = 0;
+            for (uint32_t pm = pure; pm; pm &= pm - 1) {
+                const uint32_t e = threadIdx.x + (__ffs(pm) - 1) * blockDim.x;
+                const uint32_t kv = key[e];
+                if ((kv >> 24) != 1u) continue;  // its only candidate was peeled via another cell
+                const uint32_t id = kv & 0xffffffu;
+                const uint32_t t = id / L, col = id - t * L, w = col >> 5, bit = 1u << (col & 31);
+                if (atomicOr(&claim[t * nw + w], bit) & bit) continue;  // claimed via another cell
+                const uint64_t i = b + (uint64_t)t * P.blocks;
+                const uint32_t je = e / SL;
+                const uint2 mpe = __ldg(&A.tabS[i * k + je]);
+                const float val = map_sign(mpe) * R[e];
+                for (uint32_t j = 0; j < k; j++) {
+                    // every cell of p loses it (its pure cell too: degree 0, not rescanned)
+                    if (j == je) {
+                        atomicSub(&key[e], (1u << 24) + id);
+                        continue;
+                    }
+                    const uint2 mp = __ldg(&A.tabS[i * k + j]);
+                    const uint32_t ej = (mp.x - rbase) * L + ((col + map_bias(mp)) & (L - 1));
+                    atomicAdd(&R[ej], -map_sign(mp) * val);
+                    atomicSub(&key[ej], (1u << 24) + id);
+                }
+                // outputs: slot = first slot of the row + candidates before col in the row
+                uint32_t before = 0;
+                for (uint32_t v = 0; v < w; v++) before += __popc(mask[t * nw + v]);
+                before += __popc(mask[t * nw + w] & (bit - 1u));
+                const uint64_t slot = (uint64_t)first[t] + before;
+                A.out_val[slot] = val;
+                A.out_peeled[slot] = 1;
+                A.dense[i * L + col] = val;
+                my_peeled++;
+            }
+            const uint32_t any = __syncthreads_or(my_peeled != 0u);
+            if (my_peeled) atomicAdd(&sh_peeled, my_peeled);
+            if (any && threadIdx.x == 0) sh_rounds++;
+            __syncthreads();
+        }
+        // ---- finalize: median estimate of the block's unpeeled candidates
+        for (uint32_t a = threadIdx.x; a < nrb * nw; a += blockDim.x) {
+            const uint32_t t = a / nw, w = a - t * nw;
+            uint32_t left = mask[a] & ~claim[a];
+            if (!left) continue;
+            const uint64_t i = b + (uint64_t)t * P.blocks;
+            uint32_t before = 0;
+            for (uint32_t v = 0; v < w; v++) before += __popc(mask[t * nw + v]);
+            for (; left; left &= left - 1) {
+                const uint32_t c = __ffs(left) - 1, col = 32 * w + c;
+                float v[kMaxK];
+                for (uint32_t j = 0; j < k; j++) {
+                    const uint2 mp = __ldg(&A.tabS[i * k + j]);
+                    v[j] = map_sign(mp) * R[(mp.x - rbase) * L + ((col + map_bias(mp)) & (L - 1))];
+                }
+                for (uint32_t x = 1; x < k; x++) {  // insertion sort of <= 8 values
+                    const float y = v[x];
+                    int z = (int)x - 1;
+                    while (z >= 0 && v[z] > y) { v[z + 1] = v[z]; z--; }
+                    v[z + 1] = y;
+                }
+                const float val = (k & 1) ? v[k / 2] : 0.5f * (v[k / 2 - 1] + v[k / 2]);
+                const uint64_t slot = (uint64_t)first[t] + before + __popc(mask[a] & ((1u << c) - 1u));
+                A.out_val[slot] = val;
+                A.out_peeled[slot] = 0;
+                A.dense[i * L + col] = val;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            atomicAdd(&A.ctrl->blk_peeled, (unsigned long long)sh_peeled);
+            atomicMax(&A.ctrl->blk_rounds, sh_rounds);
+        }
+        __syncthreads();
+    }
+    // the last CTA to finish writes the stats
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&A.ctrl->blk_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0 && !*(volatile uint32_t*)&A.ctrl->blk_fail) {
+        const unsigned long long np = *(volatile unsigned long long*)&A.ctrl->blk_peeled;
+        A.stats->n_peeled = np;
+        A.stats->rounds = *(volatile uint32_t*)&A.ctrl->blk_rounds;
+        A.stats->success = np == n_c ? 1 : 0;
+        A.stats->entries = 0;
+    }
+}
+
+static uint32_t rows_per_block(const KParams& P) {
+    return P.blocks ? (P.nrows + P.blocks - 1) / P.blocks : 0;
+}
+
+bool peel_blocked_fits(const KParams& P) {
+    if (!P.blocks || P.nrows == 0) return false;
+    const size_t bytes = blk_smem_words(P, rows_per_block(P)) * 4;
+    if ((uint64_t)P.k * P.S_Y * P.L > (uint64_t)kBlkThreads * kBlkCellsPerThread) return false;
+    if ((uint64_t)rows_per_block(P) * P.L >= (1u << 24)) return false;  // 24-bit local ids
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return bytes + 64 <= (size_t)optin;
+}
+
+cudaError_t launch_peel_blocked(const KParams& P, const float* counters, const uint2* tabS,
+                                const uint32_t* gmask, const uint32_t* rowoff, float* dense,
+                                uint64_t cap, float* out_val, uint8_t* out_peeled, Ctrl* ctrl,
+                                lhc_stats* stats, cudaStream_t s) {
+    BlkArgs A{};
+    A.P = P;
+    A.counters = counters;
+    A.tabS = tabS;
+    A.gmask = gmask;
+    A.rowoff = rowoff;
+    A.dense = dense;
+    A.cap = cap;
+    A.out_val = out_val;
+    A.out_peeled = out_peeled;
+    A.ctrl = ctrl;
+    A.stats = stats;
+    A.rpb = rows_per_block(P);
+    const size_t smem = blk_smem_words(P, A.rpb) * 4;
+    cudaFuncSetAttribute(k_peel_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel_blocked, kBlkThreads, smem);
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(P.blocks, (uint64_t)std::max(1, per_sm) * num_sms());
+    k_peel_blocked<<<grid, kBlkThreads, smem, s>>>(A);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace lhc

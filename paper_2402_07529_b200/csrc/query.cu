@@ -146,7 +146,7 @@ template <int KB>
 __global__ void __launch_bounds__(kQueryThreads, LHC_QUERY_MINB)
 k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS,
         uint32_t* __restrict__ gmask, uint32_t* __restrict__ cta_total, uint64_t cap,
-        uint32_t* __restrict__ out_idx, Ctrl* ctrl, lhc_stats* stats) {
+        uint32_t* __restrict__ out_idx, Ctrl* ctrl, lhc_stats* stats, uint32_t* __restrict__ rowoff) {
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t sh_warp[kQueryWarps];
     __shared__ unsigned long long sh_prefix;
@@ -234,6 +234,10 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
             }
             const uint32_t total = __shfl_sync(kFull, x, 31);
             const uint32_t ex = x - c;
+            {   // slot of the first candidate of every input row starting in this row of words
+                const uint64_t w = w0 + 32 * r + lane;
+                if (w < w_end && (w & (P.nw - 1)) == 0) rowoff[w >> P.log2nw] = (uint32_t)(run + ex);
+            }
             const uint32_t q0 = (uint32_t)((w0 + 32 * r) << 5);
             const uint32_t nzw = __ballot_sync(kFull, m[r] != 0u);
             const uint32_t maxc = __reduce_max_sync(kFull, c);
@@ -287,13 +291,13 @@ uint32_t query_max_ctas() {
 
 cudaError_t launch_query(const KParams& P, const uint32_t* bitmap, uint2* tabS, uint32_t* gmask,
                          uint32_t* cta_total, uint64_t cap, uint32_t* out_idx, Ctrl* ctrl,
-                         lhc_stats* stats, cudaStream_t s) {
+                         lhc_stats* stats, uint32_t* rowoff, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     KParams Pc = P;
     void* args[] = {(void*)&Pc,      (void*)&bitmap, (void*)&tabS, (void*)&gmask,
                     (void*)&cta_total, (void*)&cap,  (void*)&out_idx, (void*)&ctrl,
-                    (void*)&stats};
+                    (void*)&stats, (void*)&rowoff};
     cudaError_t e = P.kb == 3
         ? cudaLaunchCooperativeKernel((const void*)k_query<3>, dim3(query_grid<3>(dev)),
                                       dim3(kQueryThreads), args, 0, s)

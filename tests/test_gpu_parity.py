@@ -508,12 +508,16 @@ def blocked_params(lhc, d, nnz, W, L, B, gamma=1.5, seed=0xB10C):
     (777_777, 30_000, 4, 256, 33),         # B does not divide the row count
 ])
 @pytest.mark.parametrize("law", ["dyadic", "gauss"])
-@pytest.mark.parametrize("build", ["insert", "rows", "compact"])
+@pytest.mark.parametrize("build", ["blocked", "insert", "rows", "compact"])
 def test_blocked_sketch_pipeline(lhc, ora, d, nnz, W, L, B, law, build, monkeypatch):
     """P:L206 blocks: every row map, the bitmap, counters, candidates, flags, rounds
-    and values equal the oracle's on a blocked sketch, through every build mode of
-    the peeling state."""
-    monkeypatch.setenv("LHC_CELL_BUILD", build)
+    and values equal the oracle's on a blocked sketch — with the block-local
+    shared-memory peel (k_peel_blocked, the default for a blocked sketch) and through
+    every build mode of the global peel."""
+    if build == "blocked":
+        monkeypatch.delenv("LHC_CELL_BUILD", raising=False)
+    else:
+        monkeypatch.setenv("LHC_CELL_BUILD", build)
     p = blocked_params(lhc, d, nnz, W, L, B)
     op = ora_params(ora, p)
     xs = make_workers(d, nnz, W, 50 + B, law)
@@ -524,3 +528,35 @@ def test_blocked_sketch_pipeline(lhc, ora, d, nnz, W, L, B, law, build, monkeypa
     assert np.array_equal(U(run.sketch.bitmap), B_)
     assert_values(F(run.sketch.counters), Y, law == "dyadic")
     compare_decode(ora, dec, ref, law == "dyadic")
+
+
+@pytest.mark.parametrize("law", ["dyadic", "gauss"])
+def test_blocked_peel_falls_back_to_global(lhc, ora, law, monkeypatch):
+    """A block whose destination rows collect more input rows than the block-local
+    keys can count (> 127) hands the decode to the global peel, which produces the
+    oracle's result; so does any block in an overloaded (failing) decode."""
+    monkeypatch.delenv("LHC_CELL_BUILD", raising=False)
+    d, L, B = 1000 * 256, 256, 2          # 500 rows per block onto S = 2 rows per partition
+    p = lhc.params(d, 3 * 1024 * 64, B * 3 * 2 * L, 3, 0, L, 0xFA11, B)
+    op = ora_params(ora, p)
+    xs = make_workers(d, 800, 2, 77, law)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=2)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    _, _, ref = ora.pipeline(op, xs)
+    compare_decode(ora, dec, ref, law == "dyadic")
+
+
+@pytest.mark.parametrize("gamma", [1.25, 1.4])
+def test_blocked_peel_failure_parity(lhc, ora, gamma, monkeypatch):
+    """Near and below the per-block threshold some blocks stall: flags, rounds and the
+    median-fallback values still equal the oracle's (dyadic law: exact)."""
+    monkeypatch.delenv("LHC_CELL_BUILD", raising=False)
+    p = blocked_params(lhc, 500_000, 8_000, 3, 128, 40, gamma=gamma, seed=0xF0 + int(gamma * 100))
+    op = ora_params(ora, p)
+    xs = make_workers(500_000, 8_000, 3, 91, "dyadic")
+    run = lhc.LosslessAllReduce(p, cap_cand=500_000, local_workers=3)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    _, _, ref = ora.pipeline(op, xs)
+    compare_decode(ora, dec, ref, True)

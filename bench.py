@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--law", default="gauss")
     ap.add_argument("--index", choices=["bloom", "bitmap", "auto"], default="bloom",
                     help="Bloom filter (default), exact bitmap (P:L188), or the smaller of the two")
+    ap.add_argument("--blocks", default="0",
+                    help="0: one Count Sketch (default); N or 'auto': the sketch split into "
+                         "blocks (P:L206, NEXT-3) peeled block-locally in shared memory")
+    ap.add_argument("--L", type=int, default=1024, help="batch width (paper: 1024, P:L261)")
     ap.add_argument("--fuse-local", action="store_true",
                     help="compress a rank's workers straight into one sketch (no per-worker sketches)")
     ap.add_argument("--comm", choices=["p2p", "nvls", "nccl"], default="p2p",
@@ -234,8 +238,19 @@ def main():
     kb = {"bloom": 0, "bitmap": INDEX_BITMAP}.get(args.index)
     if kb is None:
         kb = smaller_index(wl.d, wl.density, wl.workers, gamma=args.gamma)
-    sz = lhc.size_workload(wl.d, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb)
-    p = lhc.params(wl.d, sz.m, sz.c, 3, kb, 1024, SEED)
+    nblocks = 0
+    if args.blocks != "0":
+        from paper_2402_07529_b200.sizing import size_blocked
+
+        sz, nblocks = size_blocked(wl.d, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb,
+                                   L=args.L)
+        if args.blocks != "auto":
+            nblocks = int(args.blocks)
+            S = max(1, -(-sz.c // (nblocks * 3 * args.L)))
+            sz.c = nblocks * S * 3 * args.L
+    else:
+        sz = lhc.size_workload(wl.d, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb, L=args.L)
+    p = lhc.params(wl.d, sz.m, sz.c, 3, kb, args.L, SEED, nblocks)
     cap = min(wl.d, int(sz.n_cand_expected * 1.25) + 4096)
     my_workers = lhc.pipeline.owned_workers(wl.workers, rank, world)
 
@@ -723,7 +738,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": wl.name, "d": wl.d, "density": wl.density,
                        "workers": wl.workers, "structure": wl.structure, "law": wl.law,
-                       "k": 3, "L": 1024, "m": int(p.m), "c": int(p.c), "gamma": args.gamma,
+                       "k": 3, "L": int(p.L), "m": int(p.m), "c": int(p.c), "gamma": args.gamma,
+                       "blocks": int(p.blocks),
                        "index": "bitmap" if kb == INDEX_BITMAP else "bloom",
                        "sketch_bytes": int(p.m) // 8 + 4 * int(p.c),
                        "per_worker_sketches": run.per_worker,

@@ -52,7 +52,8 @@ __host__ __device__ inline size_t blk_smem_words(const KParams& P, uint32_t rpb)
     return 2 * cb                                          // key, R
            + 2 * (size_t)rpb * P.nw                        // masks, claim bits
            + rpb                                           // first slots
-           + (size_t)P.k * P.S_Y;                          // input rows per destination row
+           + (size_t)P.k * P.S_Y                           // input rows per destination row
+           + 2 * (size_t)rpb * P.k + 1;                    // row maps (uint2) of the block's rows
 }
 
 __global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_constant__ BlkArgs A) {
@@ -67,6 +68,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_co
     uint32_t* claim = mask + (size_t)A.rpb * nw;
     uint32_t* first = claim + (size_t)A.rpb * nw;
     uint32_t* rows_per_dst = first + A.rpb;
+    const size_t maps_off = ((size_t)(rows_per_dst + k * P.S_Y - sm) + 1) & ~(size_t)1;  // 8-byte aligned
+    uint2* maps = reinterpret_cast<uint2*>(sm + maps_off);                             // [rpb][k]
+
     __shared__ uint32_t sh_peeled, sh_rounds, sh_fail;
     const uint64_t n_c = *(volatile unsigned long long*)&A.ctrl->n_cand;
     if (n_c > A.cap) return;  // overflow: the stats were set by the query
@@ -91,6 +95,10 @@ __global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_co
         }
         for (uint32_t t = threadIdx.x; t < nrb; t += blockDim.x)
             first[t] = __ldcg(A.rowoff + b + (uint64_t)t * P.blocks);
+        for (uint32_t a = threadIdx.x; a < nrb * k; a += blockDim.x) {
+            const uint32_t t = a / k, j = a - t * k;
+            maps[a] = __ldg(&A.tabS[((uint64_t)b + (uint64_t)t * P.blocks) * k + j]);
+        }
         // the block's dense ranges are zeroed (values land there later)
         for (uint32_t a = threadIdx.x; a < nrb * (L / 4); a += blockDim.x) {
             const uint32_t t = a / (L / 4), u = a - t * (L / 4);
@@ -100,11 +108,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_co
         }
         __syncthreads();
         // ---- degree bound: input rows per destination row of the block
-        for (uint32_t a = threadIdx.x; a < nrb * k; a += blockDim.x) {
-            const uint32_t t = a / k, j = a - t * k;
-            const uint64_t i = b + (uint64_t)t * P.blocks;
-            atomicAdd(&rows_per_dst[__ldg(&A.tabS[i * k + j].x) - rbase], 1u);
-        }
+        for (uint32_t a = threadIdx.x; a < nrb * k; a += blockDim.x)
+            atomicAdd(&rows_per_dst[maps[a].x - rbase], 1u);
         __syncthreads();
         for (uint32_t a = threadIdx.x; a < k * P.S_Y; a += blockDim.x)
             if (rows_per_dst[a] > kBlkMaxRows) sh_fail = 1u;
@@ -118,9 +123,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_co
             const uint32_t t = a / nw, w = a - t * nw;
             uint32_t mm = mask[a];
             if (!mm) continue;
-            const uint64_t i = b + (uint64_t)t * P.blocks;
             for (uint32_t j = 0; j < k; j++) {
-                const uint2 mp = __ldg(&A.tabS[i * k + j]);
+                const uint2 mp = maps[t * k + j];
                 const uint32_t rowl = (mp.x - rbase) * L, bias = map_bias(mp);
                 for (uint32_t m2 = mm; m2; m2 &= m2 - 1) {
                     const uint32_t col = 32 * w + (__ffs(m2) - 1);
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_co
                 if (atomicOr(&claim[t * nw + w], bit) & bit) continue;  // claimed via another cell
                 const uint64_t i = b + (uint64_t)t * P.blocks;
                 const uint32_t je = e / SL;
-                const uint2 mpe = __ldg(&A.tabS[i * k + je]);
+                const uint2 mpe = maps[t * k + je];
                 const float val = map_sign(mpe) * R[e];
                 for (uint32_t j = 0; j < k; j++) {
                     // every cell of p loses it (its pure cell too: degree 0, not rescanned)
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_co
                         atomicSub(&key[e], (1u << 24) + id);
                         continue;
                     }
-                    const uint2 mp = __ldg(&A.tabS[i * k + j]);
+                    const uint2 mp = maps[t * k + j];
                     const uint32_t ej = (mp.x - rbase) * L + ((col + map_bias(mp)) & (L - 1));
                     atomicAdd(&R[ej], -map_sign(mp) * val);
                     atomicSub(&key[ej], (1u << 24) + id);
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_co
                 const uint32_t c = __ffs(left) - 1, col = 32 * w + c;
                 float v[kMaxK];
                 for (uint32_t j = 0; j < k; j++) {
-                    const uint2 mp = __ldg(&A.tabS[i * k + j]);
+                    const uint2 mp = maps[t * k + j];
                     v[j] = map_sign(mp) * R[(mp.x - rbase) * L + ((col + map_bias(mp)) & (L - 1))];
                 }
                 for (uint32_t x = 1; x < k; x++) {  // insertion sort of <= 8 values

@@ -208,3 +208,16 @@ def size_paper_optimal(d: int, n: float, C: int = 32, gamma: float = GAMMA_DEFAU
     nc = n + eps * (d - n)
     c = max(k * L, _round_up(gamma * nc, k * L))
     return Sizing(d, m, c, k, kb, L, n, eps, nc, gamma)
+
+
+# ---- NEXT-3: blocked Count Sketch ----------------------------------------
+
+def size_blocked(d: int, density: float, workers: int, cells_per_block: int = 12288,
+                 k: int = 3, L: int = 1024, **kw) -> tuple[Sizing, int]:
+    """Sizing of a blocked sketch: the unblocked (m, c) rule, then c rounded up to B
+    blocks of k partitions of S rows (S*k*L cells per block, about cells_per_block)."""
+    s = size_workload(d, density, workers, k=k, L=L, **kw)
+    S = max(1, round(cells_per_block / (k * L)))
+    blocks = max(1, math.ceil(s.c / (S * k * L)))
+    c = blocks * S * k * L
+    return Sizing(d, s.m, c, k, s.k_bloom, L, s.n_expected, s.eps, s.n_cand_expected, s.gamma), blocks

@@ -54,6 +54,7 @@ def parse():
                     help="0: one Count Sketch (default); N or 'auto': the sketch split into "
                          "blocks (P:L206, NEXT-3) peeled block-locally in shared memory")
     ap.add_argument("--L", type=int, default=1024, help="batch width (paper: 1024, P:L261)")
+    ap.add_argument("--block-cells", type=int, default=12288, help="cells per block for --blocks auto")
     ap.add_argument("--fuse-local", action="store_true",
                     help="compress a rank's workers straight into one sketch (no per-worker sketches)")
     ap.add_argument("--comm", choices=["p2p", "nvls", "nccl"], default="p2p",
@@ -243,7 +244,7 @@ def main():
         from paper_2402_07529_b200.sizing import size_blocked
 
         sz, nblocks = size_blocked(wl.d, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb,
-                                   L=args.L)
+                                   L=args.L, cells_per_block=args.block_cells)
         if args.blocks != "auto":
             nblocks = int(args.blocks)
             S = max(1, -(-sz.c // (nblocks * 3 * args.L)))

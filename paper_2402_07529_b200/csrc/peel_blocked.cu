@@ -24,7 +24,10 @@
 
 namespace lhc {
 
-constexpr int kBlkThreads = 1024;
+#ifndef LHC_BLK_THREADS
+#define LHC_BLK_THREADS 1024
+#endif
+constexpr int kBlkThreads = LHC_BLK_THREADS;
 constexpr int kBlkCellsPerThread = 32;  // a thread's pure-cell bitmask is one word
 // key = sum (2^24 + local id): with local ids < 2^24 and at most 127 input rows per
 // destination row (so degree <= 127), degree + carry of the id sum stays < 256 and
@@ -56,7 +59,7 @@ __host__ __device__ inline size_t blk_smem_words(const KParams& P, uint32_t rpb)
            + 2 * (size_t)rpb * P.k + 1;                    // row maps (uint2) of the block's rows
 }
 
-__global__ void __launch_bounds__(kBlkThreads, 1) k_peel_blocked(const __grid_constant__ BlkArgs A) {
+__global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_constant__ BlkArgs A) {
     extern __shared__ uint32_t sm[];
     const KParams& P = A.P;
     const uint32_t k = P.k, L = P.L, nw = P.nw;

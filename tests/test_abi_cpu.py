@@ -202,3 +202,21 @@ def test_paper_optimal_sizing(lhc, density):
     assert S < 1.6 * sizing.s_min_bits(n, lam, 32)
     p = lhc.params(d, s.m, s.c, 3, s.k_bloom, 1024, 1)
     assert lhc.lhc_validate(p)
+
+
+def test_blocked_sizing(lhc):
+    """NEXT-3 sizing: c is a whole number of blocks of k partitions of S rows, about
+    cells_per_block cells each, and at least the unblocked c (same provisioning)."""
+    from paper_2402_07529_b200.sizing import size_blocked
+
+    for L in (256, 1024):
+        s, B = size_blocked(32_000_000, 0.01, 8, cells_per_block=12288, L=L)
+        base = lhc.size_workload(32_000_000, 0.01, 8, L=L)
+        S = round(12288 / (3 * L))
+        assert s.c == B * 3 * S * L and s.c >= base.c and s.c - base.c < 3 * S * L
+        assert s.m == base.m
+        p = lhc.params(32_000_000, s.m, s.c, 3, 0, L, 1, B)
+        assert lhc.lhc_validate(p)
+    c_bad = 3 * L * (7 * 100 + 3)                                   # not a multiple of 7*3*L
+    assert not lhc.lhc_validate(lhc.params(32_000_000, base.m, c_bad, 3, 0, L, 1, 7))
+    assert lhc.lhc_validate(lhc.params(32_000_000, base.m, c_bad, 3, 0, L, 1, 0))

@@ -252,7 +252,9 @@ def main():
     else:
         sz = lhc.size_workload(wl.d, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb, L=args.L)
     p = lhc.params(wl.d, sz.m, sz.c, 3, kb, args.L, SEED, nblocks)
-    cap = min(wl.d, int(sz.n_cand_expected * 1.25) + 4096)
+    # candidate capacity: n_c concentrates within ~0.5 % of its expectation (runs of 64:
+    # std ~ 64 sqrt(runs)); 5 % headroom, and stats.overflow would report a miss
+    cap = min(wl.d, int(sz.n_cand_expected * 1.05) + 4096)
     my_workers = lhc.pipeline.owned_workers(wl.workers, rank, world)
 
     trace('inputs')

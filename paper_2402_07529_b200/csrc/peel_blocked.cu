@@ -33,6 +33,9 @@ constexpr int kBlkCellsPerThread = 32;  // a thread's pure-cell bitmask is one w
 // destination row (so degree <= 127), degree + carry of the id sum stays < 256 and
 // equals 1 only when the true degree is 1
 constexpr uint32_t kBlkMaxRows = 127;
+#ifndef LHC_BLK_TIMING
+#define LHC_BLK_TIMING 0
+#endif
 
 struct BlkArgs {
     KParams P;
@@ -56,7 +59,9 @@ __host__ __device__ inline size_t blk_smem_words(const KParams& P, uint32_t rpb)
            + 2 * (size_t)rpb * P.nw                        // masks, claim bits
            + rpb                                           // first slots
            + (size_t)P.k * P.S_Y                           // input rows per destination row
-           + 2 * (size_t)rpb * P.k + 1;                    // row maps (uint2) of the block's rows
+           + 2 * (size_t)rpb * P.k + 1                     // row maps (uint2) of the block's rows
+           + (size_t)rpb * P.nw                            // block-local index of each word's first candidate
+           + cb;                                           // values of the block's candidates
 }
 
 __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_constant__ BlkArgs A) {
@@ -73,6 +78,11 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
     uint32_t* rows_per_dst = first + A.rpb;
     const size_t maps_off = ((size_t)(rows_per_dst + k * P.S_Y - sm) + 1) & ~(size_t)1;  // 8-byte aligned
     uint2* maps = reinterpret_cast<uint2*>(sm + maps_off);                             // [rpb][k]
+    uint32_t* wpre = reinterpret_cast<uint32_t*>(maps + (size_t)A.rpb * k);            // [rpb][nw]
+    float* cval = reinterpret_cast<float*>(wpre + (size_t)A.rpb * nw);                 // [cb]
+    __shared__ uint32_t sh_warp[32];
+    __shared__ uint32_t sh_nb;
+    const uint32_t cells_per_thread = (cb + blockDim.x - 1) / blockDim.x;  // <= kBlkCellsPerThread
 
     __shared__ uint32_t sh_peeled, sh_rounds, sh_fail;
     const uint64_t n_c = *(volatile unsigned long long*)&A.ctrl->n_cand;
@@ -84,6 +94,8 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
         const uint64_t cbase = (uint64_t)b * cb;           // first cell of the block
         const uint32_t rbase = b * k * P.S_Y;              // first destination row
         if (threadIdx.x == 0) { sh_peeled = 0; sh_rounds = 0; sh_fail = 0; }
+        unsigned long long tb0 = 0, tb1 = 0, tb2 = 0, tb3 = 0;
+        if (LHC_BLK_TIMING && threadIdx.x == 0) tb0 = globaltimer();
         // ---- load
         for (uint32_t e = threadIdx.x; e < cb; e += blockDim.x) {
             key[e] = 0u;
@@ -121,6 +133,7 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
             if (threadIdx.x == 0) atomicOr(&A.ctrl->blk_fail, 1u);
             continue;  // uniform
         }
+        if (LHC_BLK_TIMING && threadIdx.x == 0) tb1 = globaltimer();
         // ---- insert: (row t, word w) pairs, every set bit a candidate
         for (uint32_t a = threadIdx.x; a < nrb * nw; a += blockDim.x) {
             const uint32_t t = a / nw, w = a - t * nw;
@@ -135,12 +148,48 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
                 }
             }
         }
+        // block-local candidate index of every word's first candidate (exclusive scan
+        // of the words' popcounts: thread = a run of consecutive words)
+        {
+            const uint32_t nwords = nrb * nw;
+            const uint32_t per = (nwords + blockDim.x - 1) / blockDim.x;
+            const uint32_t w0 = threadIdx.x * per, w1 = min(nwords, w0 + per);
+            uint32_t sum = 0;
+            for (uint32_t a = w0; a < w1; a++) sum += __popc(mask[a]);
+            const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            uint32_t x = sum;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            if (lane == 31) sh_warp[warp] = x;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t run = 0;
+                for (uint32_t v = 0; v < blockDim.x / 32; v++) {
+                    const uint32_t c = sh_warp[v];
+                    sh_warp[v] = run;
+                    run += c;
+                }
+                sh_nb = run;
+            }
+            __syncthreads();
+            uint32_t run = sh_warp[warp] + x - sum;
+            for (uint32_t a = w0; a < w1; a++) {
+                wpre[a] = run;
+                run += __popc(mask[a]);
+            }
+        }
         __syncthreads();
+        // values go through shared memory (written out row by row at the end) unless the
+        // block holds more candidates than cells (such a block cannot be peeled anyway)
+        const bool staged = sh_nb <= cb;
+        if (LHC_BLK_TIMING && threadIdx.x == 0) tb2 = globaltimer();
         // ---- synchronous rounds
         for (;;) {
             // A: pure cells at the start of the round (thread-strided, <= 32 per thread)
             uint32_t pure = 0u;
-            for (uint32_t s = 0; s < kBlkCellsPerThread; s++) {
+            for (uint32_t s = 0; s < cells_per_thread; s++) {
                 const uint32_t e = threadIdx.x + s * blockDim.x;
                 if (e < cb && (key[e] >> 24) == 1u) pure |= 1u << s;
             }
@@ -169,29 +218,29 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
                     atomicAdd(&R[ej], -map_sign(mp) * val);
                     atomicSub(&key[ej], (1u << 24) + id);
                 }
-                // outputs: slot = first slot of the row + candidates before col in the row
-                uint32_t before = 0;
-                for (uint32_t v = 0; v < w; v++) before += __popc(mask[t * nw + v]);
-                before += __popc(mask[t * nw + w] & (bit - 1u));
-                const uint64_t slot = (uint64_t)first[t] + before;
-                A.out_val[slot] = val;
-                A.out_peeled[slot] = 1;
-                A.dense[i * L + col] = val;
+                const uint32_t ci = wpre[t * nw + w] + __popc(mask[t * nw + w] & (bit - 1u));
+                if (staged) {
+                    cval[ci] = val;
+                } else {  // slot = first slot of the row + candidates before col in the row
+                    const uint64_t slot = (uint64_t)first[t] + ci - wpre[t * nw];
+                    A.out_val[slot] = val;
+                    A.out_peeled[slot] = 1;
+                    A.dense[i * L + col] = val;
+                }
                 my_peeled++;
             }
+            // the barrier that ends the round (the next scan sees every update)
             const uint32_t any = __syncthreads_or(my_peeled != 0u);
             if (my_peeled) atomicAdd(&sh_peeled, my_peeled);
             if (any && threadIdx.x == 0) sh_rounds++;
-            __syncthreads();
         }
+        if (LHC_BLK_TIMING && threadIdx.x == 0) tb3 = globaltimer();
         // ---- finalize: median estimate of the block's unpeeled candidates
         for (uint32_t a = threadIdx.x; a < nrb * nw; a += blockDim.x) {
             const uint32_t t = a / nw, w = a - t * nw;
             uint32_t left = mask[a] & ~claim[a];
             if (!left) continue;
             const uint64_t i = b + (uint64_t)t * P.blocks;
-            uint32_t before = 0;
-            for (uint32_t v = 0; v < w; v++) before += __popc(mask[t * nw + v]);
             for (; left; left &= left - 1) {
                 const uint32_t c = __ffs(left) - 1, col = 32 * w + c;
                 float v[kMaxK];
@@ -206,16 +255,48 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
                     v[z + 1] = y;
                 }
                 const float val = (k & 1) ? v[k / 2] : 0.5f * (v[k / 2 - 1] + v[k / 2]);
-                const uint64_t slot = (uint64_t)first[t] + before + __popc(mask[a] & ((1u << c) - 1u));
-                A.out_val[slot] = val;
-                A.out_peeled[slot] = 0;
-                A.dense[i * L + col] = val;
+                const uint32_t ci = wpre[a] + __popc(mask[a] & ((1u << c) - 1u));
+                if (staged) {
+                    cval[ci] = val;
+                } else {
+                    const uint64_t slot = (uint64_t)first[t] + ci - wpre[t * nw];
+                    A.out_val[slot] = val;
+                    A.out_peeled[slot] = 0;
+                    A.dense[i * L + col] = val;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- outputs, word by word (consecutive threads: consecutive words of a row)
+        if (staged) {
+            for (uint32_t a = threadIdx.x; a < nrb * nw; a += blockDim.x) {
+                uint32_t mm = mask[a];
+                if (!mm) continue;
+                const uint32_t t = a / nw, w = a - t * nw;
+                const uint64_t i = b + (uint64_t)t * P.blocks;
+                const uint32_t cl = claim[a];
+                const uint64_t slot0 = (uint64_t)first[t] + wpre[a] - wpre[t * nw];
+                for (uint32_t r = 0; mm; mm &= mm - 1, r++) {
+                    const uint32_t c = __ffs(mm) - 1;
+                    const float val = cval[wpre[a] + r];
+                    A.out_val[slot0 + r] = val;
+                    A.out_peeled[slot0 + r] = (cl >> c) & 1u;
+                    A.dense[i * L + 32 * w + c] = val;
+                }
             }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             atomicAdd(&A.ctrl->blk_peeled, (unsigned long long)sh_peeled);
             atomicMax(&A.ctrl->blk_rounds, sh_rounds);
+            if (LHC_BLK_TIMING) {  // debug: summed phase durations (ns) in ctrl->t[8..12]
+                const unsigned long long tb4 = globaltimer();
+                atomicAdd(&A.ctrl->t[8], tb1 - tb0);
+                atomicAdd(&A.ctrl->t[9], tb2 - tb1);
+                atomicAdd(&A.ctrl->t[10], tb3 - tb2);
+                atomicAdd(&A.ctrl->t[11], tb4 - tb3);
+                atomicAdd(&A.ctrl->t[12], 1ull);
+            }
         }
         __syncthreads();
     }

@@ -269,6 +269,8 @@ def main():
 
         if args.comm == "nccl":
             raise SystemExit("--decode sharded needs --comm p2p or nvls")
+        if args.blocks != "0":
+            raise SystemExit("--blocks applies to the replicated decode")
         plan = shard_plan(wl.d, world, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb)
         run = lhc.ShardedAllReduce(plan, seed=SEED, local_workers=len(xs),
                                    per_worker=not args.fuse_local, device=dev, comm=args.comm)

@@ -135,10 +135,10 @@ __device__ __forceinline__ void query_chunks8_onerow(const KParams& P,
 // Each warp owns a contiguous sub-range of its CTA's chunks.  Phase 1 works on
 // chunks (lane = word) and records the warp's candidate total; phase 2 walks the
 // same sub-range 128 words at a time (four coalesced rows of 32 words, lane =
-// word): a warp scan of the word popcounts gives every word its first slot and
-// the nonzero words are expanded one at a time by the whole warp (lane = bit), so
-// the candidates leave in ascending order with coalesced stores and no lane
-// serialises over a dense word.
+// word): a warp scan of the word popcounts gives every word its first slot; the
+// row's candidates are expanded into a warp-private shared-memory buffer (each
+// lane over its own word's bits, or the whole warp one word at a time when the
+// words are dense) and leave in ascending order with coalesced stores.
 #ifndef LHC_QUERY_MINB
 #define LHC_QUERY_MINB 3
 #endif
@@ -150,6 +150,7 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t sh_warp[kQueryWarps];
     __shared__ unsigned long long sh_prefix;
+    __shared__ uint32_t sh_buf[kQueryWarps][kTile];  // one row of 32 words' candidates per warp
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
     const uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;  // chunks per CTA
@@ -215,6 +216,7 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
     unsigned long long run = sh_prefix;
     for (uint32_t v = 0; v < warp; v++) run += sh_warp[v];
     const uint32_t lt = (1u << lane) - 1u;
+    uint32_t* buf = sh_buf[warp];
     const uint64_t w_begin = wc_begin * 32, w_end = wc_end * 32;
     for (uint64_t w0 = w_begin; w0 < w_end; w0 += 128) {
         uint32_t m[4];
@@ -238,24 +240,32 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
                 const uint64_t w = w0 + 32 * r + lane;
                 if (w < w_end && (w & (P.nw - 1)) == 0) rowoff[w >> P.log2nw] = (uint32_t)(run + ex);
             }
-            const uint32_t q0 = (uint32_t)((w0 + 32 * r) << 5);
-            const uint32_t nzw = __ballot_sync(kFull, m[r] != 0u);
-            const uint32_t maxc = __reduce_max_sync(kFull, c);
-            if (maxc <= (uint32_t)__popc(nzw)) {
-                // sparse words: every lane walks its own word (at most maxc steps)
-                unsigned long long pos = run + ex;
-                for (uint32_t mm = m[r]; mm; mm &= mm - 1, pos++)
-                    if (pos < cap) out_idx[pos] = q0 + 32 * lane + (__ffs(mm) - 1);
-            } else {
-                // dense words: the warp expands one word at a time (lane = bit)
-                for (uint32_t nz = nzw; nz; nz &= nz - 1) {
-                    const uint32_t wz = __ffs(nz) - 1;
-                    const uint32_t mw = __shfl_sync(kFull, m[r], wz);
-                    const uint32_t off = __shfl_sync(kFull, ex, wz);
-                    if ((mw >> lane) & 1u) {
-                        const unsigned long long pos = run + off + __popc(mw & lt);
-                        if (pos < cap) out_idx[pos] = q0 + 32 * wz + lane;
+            if (total) {
+                const uint32_t q0 = (uint32_t)((w0 + 32 * r) << 5);
+                const uint32_t nzw = __ballot_sync(kFull, m[r] != 0u);
+                const uint32_t maxc = __reduce_max_sync(kFull, c);
+                __syncwarp();  // the previous row's copy has read the buffer
+                if (maxc <= (uint32_t)__popc(nzw)) {
+                    // sparse words: every lane walks its own word (at most maxc steps)
+                    uint32_t pos = ex;
+                    for (uint32_t mm = m[r]; mm; mm &= mm - 1, pos++)
+                        buf[pos] = q0 + 32 * lane + (__ffs(mm) - 1);
+                } else {
+                    // dense words: the warp expands one word at a time (lane = bit)
+                    for (uint32_t nz = nzw; nz; nz &= nz - 1) {
+                        const uint32_t wz = __ffs(nz) - 1;
+                        const uint32_t mw = __shfl_sync(kFull, m[r], wz);
+                        const uint32_t off = __shfl_sync(kFull, ex, wz);
+                        if ((mw >> lane) & 1u) buf[off + __popc(mw & lt)] = q0 + 32 * wz + lane;
                     }
+                }
+                __syncwarp();
+                // coalesced copy of the row's candidates to their slots
+                if (run + total <= cap) {
+                    for (uint32_t q = lane; q < total; q += 32) out_idx[run + q] = buf[q];
+                } else {
+                    for (uint32_t q = lane; q < total; q += 32)
+                        if (run + q < cap) out_idx[run + q] = buf[q];
                 }
             }
             run += total;

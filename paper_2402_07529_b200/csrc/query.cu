@@ -29,6 +29,8 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kQueryThreads = 256;  // 8 warps
 constexpr int kQueryWarps = kQueryThreads / 32;
 constexpr int kChunksPerWarp = 4;
+constexpr uint32_t kQGroupWords = 128;  // phase-2 group: 4 words per lane, 4096 coordinates
+constexpr size_t kQuerySmem = (size_t)kQueryWarps * kQGroupWords * 32 * sizeof(uint16_t);
 
 // Candidate masks of kChunksPerWarp chunks (lane = word); all lanes must call.
 // KB: compile-time number of Bloom probes (3) or 0 for a run-time k_bloom <= kMaxK.
@@ -134,11 +136,14 @@ __device__ __forceinline__ void query_chunks8_onerow(const KParams& P,
 
 // Each warp owns a contiguous sub-range of its CTA's chunks.  Phase 1 works on
 // chunks (lane = word) and records the warp's candidate total; phase 2 walks the
-// same sub-range 128 words at a time (four coalesced rows of 32 words, lane =
-// word): a warp scan of the word popcounts gives every word its first slot; the
-// row's candidates are expanded into a warp-private shared-memory buffer (each
-// lane over its own word's bits, or the whole warp one word at a time when the
-// words are dense) and leave in ascending order with coalesced stores.
+// same sub-range in groups of 128 words (4096 coordinates; lane = four
+// consecutive words, one 16-byte load): one warp scan of the lanes' popcounts
+// gives every lane its first slot, the words' candidates are written (as 12-bit
+// offsets in the group) into a warp-private shared-memory buffer — per word slot
+// lane-serially or warp-cooperatively, whichever takes fewer steps — and the
+// group's candidates leave in ascending order with coalesced stores.  (ncu: the
+// kernel is issue-bound, so phase 2 pays one scan, one pair of warp barriers and
+// one copy loop per group instead of per 32 words.)
 #ifndef LHC_QUERY_MINB
 #define LHC_QUERY_MINB 3
 #endif
@@ -150,7 +155,7 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t sh_warp[kQueryWarps];
     __shared__ unsigned long long sh_prefix;
-    __shared__ uint32_t sh_buf[kQueryWarps][kTile];  // one row of 32 words' candidates per warp
+    extern __shared__ uint16_t sh_buf[];  // per warp: one group's candidates (offsets in the group)
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
     const uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;  // chunks per CTA
@@ -216,60 +221,67 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
     unsigned long long run = sh_prefix;
     for (uint32_t v = 0; v < warp; v++) run += sh_warp[v];
     const uint32_t lt = (1u << lane) - 1u;
-    uint32_t* buf = sh_buf[warp];
+    uint16_t* buf = sh_buf + warp * kQGroupWords * 32;
     const uint64_t w_begin = wc_begin * 32, w_end = wc_end * 32;
-    for (uint64_t w0 = w_begin; w0 < w_end; w0 += 128) {
-        uint32_t m[4];
+    for (uint64_t w0 = w_begin; w0 < w_end; w0 += kQGroupWords) {
+        // lane owns words w0 + 4 lane .. + 3 (w_end - w0 is a multiple of 32)
+        const uint64_t wl = w0 + 4 * lane;
+        uint4 mv = make_uint4(0u, 0u, 0u, 0u);
+        if (wl < w_end) mv = __ldcg(reinterpret_cast<const uint4*>(gmask + wl));
+        const uint32_t m[4] = {mv.x, mv.y, mv.z, mv.w};
+        const uint32_t c = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
+        uint32_t x = c;  // inclusive warp scan
 #pragma unroll
-        for (int r = 0; r < 4; r++) {
-            const uint64_t w = w0 + 32 * r + lane;
-            m[r] = w < w_end ? __ldcg(gmask + w) : 0u;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= (uint32_t)o) x += y;
         }
+        const uint32_t total = __shfl_sync(kFull, x, 31);
+        if (total == 0) {
+            // no candidates: only the row offsets
+            if (wl < w_end) {
 #pragma unroll
-        for (int r = 0; r < 4; r++) {
-            const uint32_t c = __popc(m[r]);
-            uint32_t x = c;  // inclusive warp scan
+                for (int k = 0; k < 4; k++)
+                    if (((wl + k) & (P.nw - 1)) == 0) rowoff[(wl + k) >> P.log2nw] = (uint32_t)run;
+            }
+            continue;
+        }
+        __syncwarp();  // the previous group's copy has read the buffer
+        uint32_t pos = x - c;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(kFull, x, o);
-                if (lane >= (uint32_t)o) x += y;
-            }
-            const uint32_t total = __shfl_sync(kFull, x, 31);
-            const uint32_t ex = x - c;
-            {   // slot of the first candidate of every input row starting in this row of words
-                const uint64_t w = w0 + 32 * r + lane;
-                if (w < w_end && (w & (P.nw - 1)) == 0) rowoff[w >> P.log2nw] = (uint32_t)(run + ex);
-            }
-            if (total) {
-                const uint32_t q0 = (uint32_t)((w0 + 32 * r) << 5);
-                const uint32_t nzw = __ballot_sync(kFull, m[r] != 0u);
-                const uint32_t maxc = __reduce_max_sync(kFull, c);
-                __syncwarp();  // the previous row's copy has read the buffer
-                if (maxc <= (uint32_t)__popc(nzw)) {
-                    // sparse words: every lane walks its own word (at most maxc steps)
-                    uint32_t pos = ex;
-                    for (uint32_t mm = m[r]; mm; mm &= mm - 1, pos++)
-                        buf[pos] = q0 + 32 * lane + (__ffs(mm) - 1);
-                } else {
-                    // dense words: the warp expands one word at a time (lane = bit)
-                    for (uint32_t nz = nzw; nz; nz &= nz - 1) {
-                        const uint32_t wz = __ffs(nz) - 1;
-                        const uint32_t mw = __shfl_sync(kFull, m[r], wz);
-                        const uint32_t off = __shfl_sync(kFull, ex, wz);
-                        if ((mw >> lane) & 1u) buf[off + __popc(mw & lt)] = q0 + 32 * wz + lane;
-                    }
-                }
-                __syncwarp();
-                // coalesced copy of the row's candidates to their slots
-                if (run + total <= cap) {
-                    for (uint32_t q = lane; q < total; q += 32) out_idx[run + q] = buf[q];
-                } else {
-                    for (uint32_t q = lane; q < total; q += 32)
-                        if (run + q < cap) out_idx[run + q] = buf[q];
+        for (int k = 0; k < 4; k++) {
+            // word slot k of every lane: lane-serial over the word's bits (max_l popc
+            // steps) or, when fewer, the whole warp one nonzero word at a time (lane =
+            // bit) — runs of candidates make a few words full and the rest sparse
+            if (wl < w_end && ((wl + k) & (P.nw - 1)) == 0) rowoff[(wl + k) >> P.log2nw] = (uint32_t)(run + pos);
+            const uint32_t pk = __popc(m[k]);
+            const uint32_t nzk = __ballot_sync(kFull, m[k] != 0u);
+            const uint32_t maxk = __reduce_max_sync(kFull, pk);
+            if (maxk <= (uint32_t)__popc(nzk)) {
+                uint32_t q = pos;
+                const uint32_t base = 128 * lane + 32 * k;  // coordinate offset in the group
+                for (uint32_t mm = m[k]; mm; mm &= mm - 1, q++) buf[q] = (uint16_t)(base + (__ffs(mm) - 1));
+            } else {
+                for (uint32_t nz = nzk; nz; nz &= nz - 1) {
+                    const uint32_t wz = __ffs(nz) - 1;
+                    const uint32_t mw = __shfl_sync(kFull, m[k], wz);
+                    const uint32_t off = __shfl_sync(kFull, pos, wz);
+                    if ((mw >> lane) & 1u) buf[off + __popc(mw & lt)] = (uint16_t)(128 * wz + 32 * k + lane);
                 }
             }
-            run += total;
+            pos += pk;
         }
+        __syncwarp();
+        // coalesced copy of the group's candidates to their slots
+        const uint32_t g0 = (uint32_t)(w0 << 5);
+        if (run + total <= cap) {
+            uint32_t* o = out_idx + run;
+            for (uint32_t q = lane; q < total; q += 32) o[q] = g0 + buf[q];
+        } else {
+            for (uint32_t q = lane; q < total; q += 32)
+                if (run + q < cap) out_idx[run + q] = g0 + buf[q];
+        }
+        run += total;
     }
     // the last warp of the last CTA ends at the grand total
     if (blockIdx.x == gridDim.x - 1 && warp == kQueryWarps - 1 && lane == 0) {
@@ -286,8 +298,9 @@ template <int KB>
 static int query_grid(int dev) {
     static int cached[64] = {0};
     if (dev < 64 && cached[dev]) return cached[dev];
+    cudaFuncSetAttribute(k_query<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQuerySmem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<KB>, kQueryThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<KB>, kQueryThreads, kQuerySmem);
     int g = std::max(1, per_sm) * num_sms();
     if (dev < 64) cached[dev] = g;
     return g;
@@ -310,9 +323,9 @@ cudaError_t launch_query(const KParams& P, const uint32_t* bitmap, uint2* tabS, 
                     (void*)&stats, (void*)&rowoff};
     cudaError_t e = P.kb == 3
         ? cudaLaunchCooperativeKernel((const void*)k_query<3>, dim3(query_grid<3>(dev)),
-                                      dim3(kQueryThreads), args, 0, s)
+                                      dim3(kQueryThreads), args, kQuerySmem, s)
         : cudaLaunchCooperativeKernel((const void*)k_query<0>, dim3(query_grid<0>(dev)),
-                                      dim3(kQueryThreads), args, 0, s);
+                                      dim3(kQueryThreads), args, kQuerySmem, s);
     count_launch();
     return e;
 }

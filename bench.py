@@ -711,6 +711,7 @@ def main():
     # measured DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum of
     # one `ncu --set full` capture of this workload at N = 1, profiles/traffic.json)
     traffic = {}
+    tf = {}
     try:
         tf = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         if world == 1 and not sharded and args.comm == "p2p":
@@ -719,6 +720,24 @@ def main():
         pass
     for name in kernels:
         kernels[name]["traffic"] = traffic.get(name)
+    # the query is bound by instruction issue, not bytes (ncu: IPC 2.0-2.5 of 4, DRAM
+    # 2-7 %): warp instructions per launch (smsp__inst_executed.sum of the same capture,
+    # profiles/traffic.json "inst") against 4 issues per SM per cycle at the max SM clock
+    try:
+        inst = tf.get("inst", {}).get(wl.name + ("-bitmap" if kb == INDEX_BITMAP else ""), {}) \
+            if world == 1 and not sharded else {}
+    except Exception:
+        inst = {}
+    if "k_query" in kernels and inst.get("k_query"):
+        cs = clocks.summary()
+        mhz = cs.get("sm_max_mhz") or 1965.0
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        ipk = 4.0 * n_sm * mhz * 1e6 / 1e9  # G warp-instructions/s
+        ach_i = inst["k_query"] / (kernels["k_query"]["avg_launch_us"] * 1e-6) / 1e9
+        kernels["k_query"]["issue"] = {
+            "bound": "alu", "inst_per_launch": int(inst["k_query"]), "achieved": ach_i, "peak": ipk,
+            "unit": "G warp-instructions/s", "frac": ach_i / ipk,
+            "peak_source": f"{n_sm} SMs x 4 schedulers x {mhz:.0f} MHz (one issue per scheduler per cycle)"}
     dom = max(kernels, key=lambda k: kernels[k]["us_per_step"])
     roofline = dict(kernels[dom])
     roofline.update({"kernel": dom,

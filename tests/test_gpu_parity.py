@@ -274,6 +274,38 @@ def test_overflow_and_caps(lhc, ora):
         compare_decode(ora, dec, ref, exact=True)
 
 
+@pytest.mark.parametrize("L", [32, 64, 1024])
+def test_query_mask_patterns(lhc, ora, L):
+    """Query phase 2 works on 128-word groups (4096 coordinates), per word slot
+    lane-serially or warp-cooperatively: a fully set group, runs of 64 and 256, sparse
+    coordinates, a ragged last group (d not a multiple of 4096) and caps that cut a
+    group in the middle; candidate list (and its truncated prefix) bit-exact."""
+    d = 4096 * 37 + 1000 + 3
+    rng = rng_for(4096 + L)
+    x = np.zeros(d, np.float32)
+    x[8192:12288] = 0.25                                  # one whole group
+    for r in range(40):                                   # runs of 64 and 256
+        a = 20000 + 1500 * r
+        x[a:a + (64 if r % 2 else 256)] = -0.5
+    sp = rng.choice(d, d // 100, replace=False)           # 1 % sparse
+    x[sp] = 0.125
+    x[d - 3:] = 1.0                                       # the ragged tail
+    n = int(np.count_nonzero(x))
+    s = lhc.size_workload(d, n / d, 1, L=L)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=0xA11 + L)
+    op = ora_params(ora, p)
+    B, Y = ora.compress_dense(op, x)
+    cand = ora.query(op, B)
+    assert len(cand) >= n
+    ref = ora.decompress(op, B, Y)
+    compare_decode(ora, run_decode(lhc, p, B, Y), ref, exact=True)
+    for cap in (len(cand) - 1, len(cand) // 2 + 7, 4096 + 5):
+        dec = run_decode(lhc, p, B, Y, cap=cap)
+        st = dec.read_stats()
+        assert st["n_cand"] == len(cand) and st["overflow"] and not st["success"]
+        assert np.array_equal(U(dec.idx[:cap]), cand[:cap])
+
+
 def test_empty_and_degenerate(lhc, ora):
     L = 1024
     p = gpu_params(lhc, 5000, 3 * L, 3 * L, L=L, seed=1)

@@ -94,8 +94,10 @@ __device__ __forceinline__ void query_chunks(const KParams& P, const uint32_t* _
 
 // L = 1024 (one input row per chunk): masks of 8 chunks at once; the 8 * KB row
 // maps are hashed by 8 * KB lanes in parallel and each lane's 8 * KB destination
-// words are loaded back to back.
-template <int KB>
+// words are loaded back to back.  The rotation by bias = 32 b5 + dh: source word w
+// is destination words w + b5 and w + b5 + 1 (shuffle indices wrap mod 32) funnel-
+// shifted by dh.  FULL: all 8 chunks lie below d (no bound checks).
+template <int KB, bool FULL>
 __device__ __forceinline__ void query_chunks8_onerow(const KParams& P,
                                                      const uint32_t* __restrict__ bitmap,
                                                      uint64_t chunk0, uint64_t chunk_end,
@@ -103,33 +105,35 @@ __device__ __forceinline__ void query_chunks8_onerow(const KParams& P,
     uint2 mine = make_uint2(0u, 0u);
     if (lane < 8 * KB) {
         const uint32_t cb = lane / KB, j = lane - cb * KB;
-        if (chunk0 + cb < chunk_end) mine = dom_map(P, 1, j, chunk0 + cb);
+        if (FULL || chunk0 + cb < chunk_end) mine = dom_map(P, 1, j, chunk0 + cb);
     }
-    uint32_t dword[8][KB], bias[8][KB];
+    uint32_t dword[8][KB], rot[8][KB];
 #pragma unroll
     for (int cb = 0; cb < 8; cb++) {
 #pragma unroll
         for (int j = 0; j < KB; j++) {
             const uint32_t rx = __shfl_sync(kFull, mine.x, cb * KB + j);
-            const uint32_t ry = __shfl_sync(kFull, mine.y, cb * KB + j);
-            bias[cb][j] = ry & 0x7fffffffu;
-            dword[cb][j] = chunk0 + cb < chunk_end ? __ldg(bitmap + (uint64_t)rx * 32 + lane) : 0u;
+            // bias < L = 1024 in the low bits, the sign in bit 31: bits 5..9 are b5,
+            // bits 0..4 dh (the funnel shift and the shuffle index use only those)
+            rot[cb][j] = __shfl_sync(kFull, mine.y, cb * KB + j);
+            dword[cb][j] = (FULL || chunk0 + cb < chunk_end) ? __ldg(bitmap + (uint64_t)rx * 32 + lane) : 0u;
         }
     }
 #pragma unroll
     for (int cb = 0; cb < 8; cb++) {
-        uint32_t res = chunk0 + cb < chunk_end ? kFull : 0u;
+        uint32_t res = (FULL || chunk0 + cb < chunk_end) ? kFull : 0u;
 #pragma unroll
         for (int j = 0; j < KB; j++) {
-            const uint32_t db = (32 * lane + bias[cb][j]) & 1023u;
-            const uint32_t dw = db >> 5, dh = db & 31;
-            const uint32_t lo = __shfl_sync(kFull, dword[cb][j], dw);
-            const uint32_t hi = __shfl_sync(kFull, dword[cb][j], (dw + 1) & 31);
-            res &= dh ? (lo >> dh) | (hi << (32 - dh)) : lo;
+            const uint32_t src = lane + (rot[cb][j] >> 5);
+            const uint32_t lo = __shfl_sync(kFull, dword[cb][j], src);
+            const uint32_t hi = __shfl_sync(kFull, dword[cb][j], src + 1);
+            res &= __funnelshift_r(lo, hi, rot[cb][j]);
         }
-        const uint64_t q0 = ((chunk0 + cb) * 32 + lane) << 5;  // clear coordinates >= d
-        if (q0 >= P.d) res = 0u;
-        else if (q0 + 32 > P.d) res &= (1u << (uint32_t)(P.d - q0)) - 1u;
+        if (!FULL) {
+            const uint64_t q0 = ((chunk0 + cb) * 32 + lane) << 5;  // clear coordinates >= d
+            if (q0 >= P.d) res = 0u;
+            else if (q0 + 32 > P.d) res &= (1u << (uint32_t)(P.d - q0)) - 1u;
+        }
         out[cb] = res;
     }
 }
@@ -178,7 +182,10 @@ k_query(KParams P, const uint32_t* __restrict__ bitmap, uint2* __restrict__ tabS
     if (KB != 0 && P.L == 1024) {
         for (uint64_t c0 = wc_begin; c0 < wc_end; c0 += 8) {
             uint32_t m[8];
-            query_chunks8_onerow<KB ? KB : 1>(P, bitmap, c0, wc_end, lane, m);
+            if (c0 + 8 <= wc_end && (c0 + 8) * kTile <= (uint64_t)P.d)
+                query_chunks8_onerow<KB ? KB : 1, true>(P, bitmap, c0, wc_end, lane, m);
+            else
+                query_chunks8_onerow<KB ? KB : 1, false>(P, bitmap, c0, wc_end, lane, m);
 #pragma unroll
             for (int cb = 0; cb < 8; cb++)
                 if (c0 + cb < wc_end) {

@@ -366,6 +366,34 @@ def test_pipeline_exact_bitmap(lhc, ora, d, nnz, W, L, law):
     compare_decode(ora, dec, ref, law == "dyadic")
 
 
+@pytest.mark.parametrize("frac", [0.70, 0.80, 0.856, 0.90, 0.95])
+def test_vgg_table1_density_recovery_sweep(lhc, ora, frac):
+    """Fig. 3-style single-GPU recovery at VGG19's Table 1 sparsity (30.4 % zeros,
+    P:L322-344): one worker, exact bitmap index, counter array swept through c/d
+    around the 85.6 % threshold. Below it the peel stalls and the median
+    fallback decides values; every flag, round count and value must still equal
+    the oracle's (dyadic values: bit-exact)."""
+    from paper_2402_07529_b200.sizing import INDEX_BITMAP
+
+    d, L = 1 << 20, 1024
+    nnz = int(round(0.696 * d))
+    s = lhc.size_workload(d, nnz / d, 1, L=L, k_bloom=INDEX_BITMAP)
+    c = 3 * L * max(1, int(round(frac * d / (3 * L))))
+    p = gpu_params(lhc, d, s.m, c, kb=INDEX_BITMAP, L=L, seed=0x344 + int(frac * 1000))
+    op = ora_params(ora, p)
+    xs = make_workers(d, nnz, 1, 344, "dyadic")
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=1)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(op, xs)
+    assert np.array_equal(U(run.sketch.bitmap), B)
+    st = compare_decode(ora, dec, ref, exact=True)
+    if frac >= 0.95:
+        assert st["success"]
+    if frac <= 0.70:
+        assert not st["success"]
+
+
 # ------------------------------------------------- BASELINE.json full sizes --
 
 FULL = [

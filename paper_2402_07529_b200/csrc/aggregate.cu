@@ -94,7 +94,16 @@ __global__ void __launch_bounds__(256) k_clear(const __grid_constant__ ClearBatc
     for (uint64_t u = tid; u < na; u += stride)
         asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(a + u), "r"(0u),
                      "l"(pol) : "memory");
-    for (uint64_t u = tid; u < nb; u += stride)
+    // bitmap words: 16-byte stores when the bitmap is 16-byte aligned, then the < 4-word tail
+    uint64_t head = 0;
+    if ((reinterpret_cast<uintptr_t>(b) & 15) == 0) {
+        head = nb & ~uint64_t(3);
+        uint4* b4 = reinterpret_cast<uint4*>(b);
+        for (uint64_t u = tid; u < head / 4; u += stride)
+            asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %1, %1, %1}, %2;" ::"l"(b4 + u),
+                         "r"(0u), "l"(pol) : "memory");
+    }
+    for (uint64_t u = head + tid; u < nb; u += stride)
         asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(b + u), "r"(0u), "l"(pol)
                      : "memory");
 }

@@ -27,9 +27,12 @@
  *
  * Pinning status (see tests/test_oracle_*.py and DESIGN.md §Oracle pins):
  *   ora_mix64            pinned: published SplitMix64 output vector
- *   ora_hash / maps      parity unpinned vs the paper (the paper gives no hash,
- *                        P:L175); pinned by statistical invariants
- *                        (uniform bias/sign/row, bijective rotation)
+ *   ora_hash / maps      the paper gives no hash: pinned to the
+ *                        written spec of SURVEY.md §8c (its three hand-computed H
+ *                        values), the frozen table tests/golden/rowmap.json
+ *                        (packing, sign bit, bias, row reduction), and
+ *                        statistical invariants (uniform bias/sign/row,
+ *                        bijective rotation)
  *   ora_compress_*       pinned: homomorphism, single-insert identity, full-row
  *                        rotation bijection, partition sums
  *   ora_aggregate        pinned: OR/sum laws on independent inputs
@@ -37,9 +40,13 @@
  *                        filter is sparse, false-positive rate vs closed form
  *   ora_peel_core        pinned: Fig. 1 worked example, brute-force
  *                        2-core on tiny inputs, chain round counts
- *   ora_finalize         pinned: hand-computed medians, unbiasedness
+ *   ora_finalize         pinned: hand-computed medians, unbiasedness,
+ *                        a hand-built partial peel whose residual medians differ
+ *                        from the medians over Y (reading R11)
  *   ora_decompress       pinned: losslessness (exact sum) under the dyadic law
- *                        (P:L66), success phase transition
+ *                        (P:L66), success phase transition, the
+ *                        fallback over the residual of a stalled decode,
+ *                        recomputed independently (reading R11)
  */
 #include <stdint.h>
 #include <stdlib.h>

@@ -66,19 +66,26 @@ def assert_values(gpu, ref, exact):
 # ---------------------------------------------------------------- hash kernel --
 
 @pytest.mark.parametrize("L", [32, 128, 1024])
-def test_hash_rows_bit_exact(lhc, ora, L):
-    p = gpu_params(lhc, 5_000_000, 3 * L * 1117, 3 * L * 733, L=L, seed=0xDEADBEEF12345)
-    op = ora_params(ora, p)
+def test_hash_rows_bit_exact(lhc, L):
+    # the frozen row-map table (tests/golden/rowmap.json, written by
+    # tools/make_golden_rowmap.py from oracle/ only; the oracle is pinned to it
+    # in tests/test_oracle.py::test_row_map_golden_table)
+    import json
+    import os
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "rowmap.json")))
+    (t,) = [t for t in g["tables"] if t["L"] == L and t["d"] == 5_000_000]
+    p = gpu_params(lhc, t["d"], 3 * L * t["S_B"], 3 * L * t["S_Y"], L=L, seed=t["seed"])
     n = 3000
     for dom in (0, 1):
         out = torch.empty(2 * n * 3, dtype=torch.int32, device="cuda")
         lhc.sketch_hash_rows(p, dom, n, out)
         got = U(out).reshape(n, 3, 2)
-        for i in range(0, n, 7):
-            for j in range(3):
-                row, bias, sign = ora.row_map(op, dom, j, i)
-                assert got[i, j, 0] == row
-                assert got[i, j, 1] == (bias | ((1 << 31) if sign < 0 else 0))
+        ent = [e for e in t["entries"] if e[0] == dom]
+        assert len(ent) == 3 * len(range(0, n, 7))
+        for _, j, i, row, bias, sign in ent:
+            assert got[i, j, 0] == row
+            assert got[i, j, 1] == (bias | ((1 << 31) if sign < 0 else 0))
 
 
 # ------------------------------------------------------------------ compress --

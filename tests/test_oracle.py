@@ -54,6 +54,43 @@ def test_row_map_statistics(ora):
                 assert abs(frac - 0.5) < 4 * 0.5 / math.sqrt(n)
 
 
+def test_hash_survey_golden_values(ora):
+    # SURVEY.md §8c step 2 (the written hash spec; the paper gives none, P:L175,
+    # P:L230) computed these three values from the spec, independently of the
+    # oracle: dom and j occupy bits 56 and 48 of the packed key.
+    assert ora.hash64(0, 0, 0, 0) == 0x48218226FF3CD4BF
+    assert ora.hash64(0, 1, 0, 0) == 0x8B793569A9EFDF25
+    assert ora.hash64(0xDEADBEEF, 0, 2, 12345) == 0x1563224AB3881EA0
+    # and the row map fields of H(0, 0, 0, 0) the survey lists: bias 191 (H & 1023),
+    # sign +1 (bit 16 of H clear)
+    L, S = 1024, 5218
+    p = P(ora, d=143_000_000, m=3 * S * L, c=3 * S * L, L=L, seed=0)
+    row, bias, sign = ora.row_map(p, 0, 0, 0)
+    assert (bias, sign) == (191, 1)
+    assert row == (0x48218226 * S) >> 32
+
+
+def test_row_map_golden_table(ora):
+    # The frozen table (tests/golden/rowmap.json, written once by
+    # tools/make_golden_rowmap.py and shared with the GPU hash test): packing
+    # (j<<48, dom<<56), sign bit 16, bias mask and row reduction per partition.
+    g = json.load(open(os.path.join(GOLDEN, "rowmap.json")))
+    for s, dom, j, i, H in g["hash"]:
+        assert ora.hash64(s, dom, j, i) == H, (s, dom, j, i)
+    n_neg = n_17 = 0
+    for t in g["tables"]:
+        p = ora.params(t["d"], t["k_bloom"] * t["S_B"] * t["L"], t["k"] * t["S_Y"] * t["L"],
+                       t["k"], t["k_bloom"], t["L"], t["seed"])
+        for dom, j, i, row, bias, sign in t["entries"]:
+            assert ora.row_map(p, dom, j, i) == (row, bias, sign), (t["L"], dom, j, i)
+            if dom == 0:
+                H = ora.hash64(t["seed"], 0, j, i)
+                n_neg += sign < 0
+                n_17 += ((H >> 16) & 1) != ((H >> 17) & 1)
+    # the table has power against a sign taken from a neighbouring bit
+    assert n_neg > 100 and n_17 > 100
+
+
 def test_sketch_and_bloom_maps_independent(ora):
     # Reading R1: domain separation; identical maps would make the Bloom false
     # positives sit exactly on occupied counter rows.
@@ -329,6 +366,58 @@ def test_unpeelable_pair_median_fallback(ora):
     assert r.rounds == 0 and not r.peeled.any()
     # item a: median(4, 2, 4) = 4; item b: median(4, -2, 4) = 4
     assert r.val.tolist() == [4.0, 4.0]
+
+
+def test_partial_peel_fallback_is_residual_median(ora):
+    # Reading R11 ("Estimate the not recovered parameters of X from Y" after
+    # the peel has deducted the recovered ones from Y).  Hand-built
+    # incidence: z -> {2, 3, 4} peels in round 1 (cells 3 and 4 hold only z; the
+    # lowest j, cell 3, gives its value); a -> {0, 1, 2} (+,+,+) and
+    # b -> {0, 1, 2} (+,-,-) share all three cells: a 2-core, estimated.
+    # a = 1, b = 2, z = 10:  Y = [3, -1, 1 - 2 + 10 = 9, 10, 10];
+    # residual after z:      R = [3, -1, -1, 0, 0].
+    # a: median(+3, -1, -1) = -1   (over Y it would be median(3, -1, 9) = 3)
+    # b: median(+3, +1, +1) = +1   (over Y: median(3, 1, -9) = 1)
+    cells = np.array([[0, 1, 2], [0, 1, 2], [2, 3, 4]], np.uint64)
+    signs = np.array([[1, 1, 1], [1, -1, -1], [1, 1, 1]], np.int8)
+    Y = np.array([3.0, -1.0, 9.0, 10.0, 10.0])
+    r = ora.peel_core(cells, signs, Y)
+    assert r.rounds == 1
+    assert r.peeled.tolist() == [False, False, True]
+    assert r.round_of.tolist() == [0, 0, 1]
+    assert r.residual.tolist() == [3.0, -1.0, -1.0, 0.0, 0.0]
+    assert r.val.tolist() == [-1.0, 1.0, 10.0]
+
+
+def test_decompress_fallback_uses_the_residual(ora):
+    # The same reading through the whole Phase II (ora_decompress): an
+    # under-provisioned sketch (c = 288 cells for ~337 candidates) stalls after a
+    # few rounds.  Independently of the oracle's peel and finalize: peeled values
+    # are the true ones (exact, dyadic law), the residual is Y minus their signed
+    # contributions at their cells, and every unpeeled candidate's value is the
+    # median over j of g_j * residual.
+    d, L, S, seed = 4096, 32, 3, 8
+    p = ora.params(d, 3 * 32 * 40, 3 * L * S, 3, 3, L, seed)
+    rng = rng_for(seed)
+    idx = support(rng, d, 300, "uniform")
+    x = np.zeros(d, np.float32)
+    x[idx] = values(rng, len(idx), "dyadic")
+    B, Y, dec = ora.pipeline(p, [x])
+    assert 0 < dec.peeled.sum() < len(dec.cand) and not dec.stats.success
+    truth = x[dec.cand].astype(np.float64)
+    assert np.array_equal(dec.val[dec.peeled], truth[dec.peeled])
+    maps = [[ora.cell(p, j, int(q)) for j in range(3)] for q in dec.cand]
+    R = Y.copy()
+    for s in np.flatnonzero(dec.peeled):
+        for e, g in maps[s]:
+            R[e] -= g * truth[s]
+    differs = 0
+    for s in np.flatnonzero(~dec.peeled):
+        est_R = np.median([g * R[e] for e, g in maps[s]])
+        est_Y = np.median([g * Y[e] for e, g in maps[s]])
+        assert dec.val[s] == est_R
+        differs += est_R != est_Y
+    assert differs > 10  # the case separates the residual from the original Y
 
 
 def test_even_k_median_is_mean_of_middle_pair(ora):

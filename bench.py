@@ -8,7 +8,7 @@ GPUs with the NVLink P2P sketch_allreduce), and every rank decodes the aggregate
 into the dense sum.  Metric (BASELINE.json): aggregated gradient elements/s =
 d / T_step, d counted once however many workers (footnote P:L367).
 
-    python bench.py [--gpus N --steps K --warmup W --config ncf]
+    python bench.py [--gpus N --steps K --warmup W --config vgg]
     torchrun --nproc-per-node N bench.py --gpus N ...
     python bench.py --impl reference ...     # the CPU oracle, timed as it stands
 
@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="ncf", help="tiny|ncf|lstm|bert|vgg")
+    ap.add_argument("--config", default="vgg",
+                    help="tiny|ncf|lstm|bert|vgg (default: VGG19-shaped, the largest single-GPU "
+                         "config: d = 143 M, 1 %%, W = 8)")
     ap.add_argument("--density", type=float, default=None)
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--gamma", type=float, default=1.30)
@@ -174,9 +176,32 @@ def run_reference(args, wl, rank):
             "config": {"workload": wl.name, "d": wl.d, "density": wl.density,
                        "workers": wl.workers, "structure": wl.structure},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, **host_cpu(),
+                             "threads": "1 (the oracle is single-threaded C)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     return line
+
+
+def host_cpu():
+    """Host core count and CPU model of the box the oracle runs on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    if model is None:
+        try:
+            for line in open("/proc/cpuinfo"):
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        except Exception:
+            pass
+    return {"host_cores": os.cpu_count(), "host_cpu": model or "unknown"}
 
 
 def sample_workload(wl, frac):
@@ -783,6 +808,11 @@ def main():
             "decode": stats,
         }
         print(json.dumps(line), flush=True)
+    # a step whose decode overflowed its candidate capacity or stalled timed a
+    # truncated peel: the line above records it, the exit code rejects it
+    bad = torch.tensor([0 if stats["success"] and not stats["overflow"] else 1], device=dev)
+    if world > 1:
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
     if comm is not None:
         comm.close()
     if sharded:
@@ -790,6 +820,10 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if int(bad.item()):
+        print(f"bench: decode failed (success={stats['success']}, overflow={stats['overflow']}); "
+              "the timed steps are not a valid measurement", file=sys.stderr, flush=True)
+        sys.exit(3)
 
 
 if __name__ == "__main__":

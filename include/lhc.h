@@ -141,9 +141,12 @@ int sketch_compress_batch(const lhc_params* p, int n, const float* const* xs, co
 
 /* Same from a COO gradient: idx[nnz] (each < d, distinct), val[nnz].  Every
  * listed entry is inserted, including val == 0 (the index describes the listed
- * support).  Accumulates like sketch_compress. */
+ * support).  Accumulates like sketch_compress.  An entry with idx >= d is a
+ * data-dependent error: it is skipped (nothing is written for it) and counted
+ * into *bad_out (device, nullable; accumulated, the caller zeroes it). */
 int sketch_compress_coo(const lhc_params* p, uint64_t nnz, const uint32_t* idx,
-                        const float* val, uint32_t* bitmap, float* counters, void* stream);
+                        const float* val, uint32_t* bitmap, float* counters,
+                        unsigned long long* bad_out, void* stream);
 
 /* ---- aggregation (Alg. 1: Y <- sum Y, B <- OR B) ---------------- */
 
@@ -195,7 +198,11 @@ void lhc_comm_destroy(lhc_comm* comm);
  *       cap_items) are pushed to every peer, and every other shard's range of
  *       dense[d] is overwritten with exactly the values its owner decoded
  *       (0 elsewhere).  Every rank ends with the identical dense sum.  idx, val
- *       and dense must be 16-byte aligned.
+ *       and dense must be 16-byte aligned.  If an owner's *n_items exceeds
+ *       cap_items (its decode overflowed and did not run), it publishes an
+ *       overflow mark instead of its list and EVERY rank, the owner included,
+ *       fills that shard's range of dense with NaN: a failed shard is visible on
+ *       all ranks, never silently stale.
  * A sharded communicator is created by lhc_shard_comm_create (same handle
  * exchange as lhc_comm_create) and released by lhc_comm_destroy; calling
  * sketch_allreduce on it, or the sharded calls on a plain one, is LHC_EINVAL.

@@ -104,7 +104,7 @@ def lib() -> ctypes.CDLL:
             "sketch_hash_rows": (i32, [P, u32, u64, vp, vp]),
             "sketch_clear": (i32, [P, vp, vp, vp]),
             "sketch_compress": (i32, [P, vp, vp, vp, vp, vp]),
-            "sketch_compress_coo": (i32, [P, u64, vp, vp, vp, vp, vp]),
+            "sketch_compress_coo": (i32, [P, u64, vp, vp, vp, vp, vp, vp]),
             "sketch_aggregate": (i32, [P, i32, vp, vp, vp, vp, vp]),
             "lhc_comm_layout": (i32, [P, ctypes.POINTER(sz), ctypes.POINTER(sz),
                                       ctypes.POINTER(sz), ctypes.POINTER(sz)]),
@@ -241,14 +241,18 @@ def sketch_clear_batch(p: lhc_params, bitmaps, counters, stream=None):
 
 
 def sketch_compress_coo(p: lhc_params, idx: torch.Tensor, val: torch.Tensor,
-                        bitmap: torch.Tensor, counters: torch.Tensor, stream=None):
+                        bitmap: torch.Tensor, counters: torch.Tensor,
+                        bad_out: torch.Tensor | None = None, stream=None):
+    """bad_out (int64[1] on the device, nullable) accumulates the number of entries
+    with idx >= d, which are skipped."""
     nnz = idx.numel()
     if val.numel() != nnz:
         raise ValueError("idx and val differ in length")
     _check("sketch_compress_coo", lib().sketch_compress_coo(
         ctypes.byref(p), nnz, _dev(idx, torch.int32, nnz, "idx"),
         _dev(val, torch.float32, nnz, "val"), _dev(bitmap, torch.int32, p.words, "bitmap"),
-        _dev(counters, torch.float32, p.c, "counters"), _stream(stream)))
+        _dev(counters, torch.float32, p.c, "counters"), _dev(bad_out, torch.int64, 1, "bad_out"),
+        _stream(stream)))
 
 
 def sketch_aggregate(p: lhc_params, bitmaps, counters, out_bitmap: torch.Tensor,

@@ -125,6 +125,7 @@ WsLayout ws_layout(const KParams& P, uint64_t cap) {
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+static bool aligned4(const void* p) { return ((uintptr_t)p & 3u) == 0; }
 
 }  // namespace lhc
 
@@ -160,6 +161,7 @@ int sketch_clear(const lhc_params* p, uint32_t* bitmap, float* counters, void* s
     reset_launches();
     if (int rc = validate(p)) return rc;
     if (!bitmap || !counters) return set_error(LHC_EINVAL, "NULL sketch buffer");
+    if (!aligned16(counters)) return set_error(LHC_EINVAL, "counters must be 16-byte aligned");
     launch_clear(1, &bitmap, p->m / 32, &counters, p->c, (cudaStream_t)stream);
     return check_launch("sketch_clear");
 }
@@ -225,13 +227,16 @@ int sketch_compress_batch(const lhc_params* p, int n, const float* const* xs, co
 }
 
 int sketch_compress_coo(const lhc_params* p, uint64_t nnz, const uint32_t* idx,
-                        const float* val, uint32_t* bitmap, float* counters, void* stream) {
+                        const float* val, uint32_t* bitmap, float* counters,
+                        unsigned long long* bad_out, void* stream) {
     reset_launches();
     if (int rc = validate(p)) return rc;
     if (nnz && (!idx || !val)) return set_error(LHC_EINVAL, "NULL idx/val");
     if (!bitmap || !counters) return set_error(LHC_EINVAL, "NULL sketch buffer");
     if (nnz > p->d) return set_error(LHC_EINVAL, "nnz > d");
-    launch_compress_coo(kparams(p), nnz, idx, val, bitmap, counters, (cudaStream_t)stream);
+    if (nnz && (!aligned4(idx) || !aligned4(val) || !aligned4(counters) || !aligned4(bitmap)))
+        return set_error(LHC_EINVAL, "idx, val, bitmap and counters must be 4-byte aligned");
+    launch_compress_coo(kparams(p), nnz, idx, val, bitmap, counters, bad_out, (cudaStream_t)stream);
     return check_launch("sketch_compress_coo");
 }
 

@@ -284,6 +284,15 @@ __global__ void __launch_bounds__(256) k_reduce_scatter(ShArgs A) {
     }
 }
 
+constexpr uint32_t kOverflowMark = 0xFFFFFFFFu;
+
+// dense[q*w, min(d, (q+1)*w)) = NaN: shard q's decode overflowed its capacity
+__device__ __forceinline__ void fill_shard_nan(float* dense, int q, uint64_t w, uint32_t d,
+                                               uint64_t gtid, uint64_t gstride) {
+    const uint64_t lo = (uint64_t)q * w, hi = min((uint64_t)d, lo + w);
+    for (uint64_t i = lo + gtid; i < hi; i += gstride) dense[i] = __int_as_float(0x7fc00000);
+}
+
 template <int G>
 __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
     cg::grid_group grid = cg::this_grid();
@@ -291,7 +300,11 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
     const uint32_t epoch = *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot);
     const uint32_t par = *(volatile uint32_t*)(A.sig[A.rank] + kAgCountSlot) & 1u;
-    const uint64_t n = min((uint64_t)*A.n_items, A.cap);
+    // an overflowed own decode (n_items > cap: the peel did not run, the list is
+    // stale) publishes kOverflowMark instead of a list; every rank then fills that
+    // shard of its dense output with NaN, so the failure is visible everywhere
+    const bool own_over = *A.n_items > A.cap;
+    const uint64_t n = own_over ? 0 : *A.n_items;
     // A gather slot holds cap indices then cap values (cap a multiple of 4): the
     // decoded list travels as two 16-byte-vector streams.
     const uint64_t nv = n / 4;
@@ -319,7 +332,8 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
                 slot[i] = __ldcg(A.idx + i);
                 slot[A.cap + i] = __float_as_uint(__ldcg(A.val + i));
             }
-            if (rtid == 0) A.sig[q][kGatherCountSlot + par * kMaxRanks + A.rank] = (uint32_t)n;
+            if (rtid == 0)
+                A.sig[q][kGatherCountSlot + par * kMaxRanks + A.rank] = own_over ? kOverflowMark : (uint32_t)n;
         }
     }
     if (!pusher || half == 0) {
@@ -335,11 +349,15 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
     }
     sh_barrier<G>(grid, A, epoch + 1);
 #pragma unroll 1
+    if (own_over) fill_shard_nan(A.dense, A.rank, A.shard_width, A.d, gtid, gstride);
     for (int dd = 1; dd < G; dd++) {
         const int q = (A.rank + dd) % G;
-        const uint64_t nq = min((uint64_t)*(volatile uint32_t*)(A.sig[A.rank] + kGatherCountSlot +
-                                                               par * kMaxRanks + q),
-                                A.cap);
+        const uint32_t cnt = *(volatile uint32_t*)(A.sig[A.rank] + kGatherCountSlot + par * kMaxRanks + q);
+        if (cnt == kOverflowMark) {
+            fill_shard_nan(A.dense, q, A.shard_width, A.d, gtid, gstride);
+            continue;
+        }
+        const uint64_t nq = min((uint64_t)cnt, A.cap);
         const uint32_t* slot = reinterpret_cast<const uint32_t*>(A.gather[A.rank] + ((uint64_t)par * G + q) * A.cap);
         const uint4* si = reinterpret_cast<const uint4*>(slot);
         const uint4* sv = reinterpret_cast<const uint4*>(slot + A.cap);
@@ -848,7 +866,8 @@ __global__ void __launch_bounds__(256) k_allgather_nvls(NvArgs A) {
     const uint32_t epoch = *(volatile uint32_t*)(A.sig_uc + 16);
     const uint32_t par = *(volatile uint32_t*)(A.sig_uc + 17) & 1u;
     const int G = A.world;
-    const uint64_t n = min((uint64_t)*A.n_items, A.cap);
+    const bool own_over = *A.n_items > A.cap;  // as in k_allgather_decoded
+    const uint64_t n = own_over ? 0 : *A.n_items;
     const uint64_t slot_bytes = A.cap * 8;
     {
         const uint64_t off = A.gather_off + ((uint64_t)par * G + A.rank) * slot_bytes;
@@ -870,7 +889,8 @@ __global__ void __launch_bounds__(256) k_allgather_nvls(NvArgs A) {
             mm_st_v4(dv + i0, b);
         }
         if (gtid == 0)
-            mm_st_u32(reinterpret_cast<uint32_t*>(A.sig_mc) + 64 + par * kMaxRanks + A.rank, (uint32_t)n);
+            mm_st_u32(reinterpret_cast<uint32_t*>(A.sig_mc) + 64 + par * kMaxRanks + A.rank,
+                      own_over ? kOverflowMark : (uint32_t)n);
     }
     {
         const uint64_t lo = (uint64_t)A.rank * A.shard_width;
@@ -882,9 +902,15 @@ __global__ void __launch_bounds__(256) k_allgather_nvls(NvArgs A) {
         for (uint64_t i = max(hi, 4 * e4) + gtid; i < A.d; i += gstride) A.dense[i] = 0.f;
     }
     nv_barrier(grid, A, (epoch + 1) * (uint32_t)A.world);
+    if (own_over) fill_shard_nan(A.dense, A.rank, A.shard_width, A.d, gtid, gstride);
     for (int dd = 1; dd < G; dd++) {
         const int q = (A.rank + dd) % G;
-        const uint64_t nq = min((uint64_t)*(volatile uint32_t*)(A.sig_uc + 64 + par * kMaxRanks + q), A.cap);
+        const uint32_t cnt = *(volatile uint32_t*)(A.sig_uc + 64 + par * kMaxRanks + q);
+        if (cnt == kOverflowMark) {
+            fill_shard_nan(A.dense, q, A.shard_width, A.d, gtid, gstride);
+            continue;
+        }
+        const uint64_t nq = min((uint64_t)cnt, A.cap);
         const char* slot = A.uc + A.gather_off + ((uint64_t)par * G + q) * slot_bytes;
         const uint4* si = reinterpret_cast<const uint4*>(slot);
         const uint4* sv = reinterpret_cast<const uint4*>(slot + A.cap * 4);

@@ -293,17 +293,22 @@ void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned lo
 
 // ---------------------------------------------------------------------------
 // COO compression: one thread per listed entry; bits are merged per warp when
-// lanes hit the same word (sorted indices make neighbours share rows).
+// lanes hit the same word (sorted indices make neighbours share rows).  An
+// entry with idx >= d is skipped and counted into *bad_out (one atomic per warp).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
 k_compress_coo(KParams P, uint64_t nnz, const uint32_t* __restrict__ idx,
                const float* __restrict__ val, uint32_t* __restrict__ bitmap,
-               float* __restrict__ counters) {
+               float* __restrict__ counters, unsigned long long* bad_out) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < nnz; base += stride) {
         const uint64_t s = base + threadIdx.x;
-        const bool live = s < nnz;
+        bool live = s < nnz;
         uint32_t p = live ? idx[s] : 0u;
+        const bool bad = live && p >= P.d;
+        const uint32_t nbad = __popc(__ballot_sync(0xffffffffu, bad));
+        if (nbad && bad_out && (threadIdx.x & 31) == 0) atomicAdd(bad_out, (unsigned long long)nbad);
+        if (bad) { live = false; p = 0u; }
         float xv = live ? val[s] : 0.f;
         const uint64_t i = p >> P.log2L;
         const uint32_t t = p & (P.L - 1);
@@ -329,10 +334,11 @@ k_compress_coo(KParams P, uint64_t nnz, const uint32_t* __restrict__ idx,
 }
 
 void launch_compress_coo(const KParams& P, uint64_t nnz, const uint32_t* idx, const float* val,
-                         uint32_t* bitmap, float* counters, cudaStream_t s) {
+                         uint32_t* bitmap, float* counters, unsigned long long* bad_out,
+                         cudaStream_t s) {
     if (nnz == 0) return;
     uint32_t blocks = (uint32_t)std::min<uint64_t>((nnz + 255) / 256, (uint64_t)num_sms() * 8);
-    k_compress_coo<<<blocks, 256, 0, s>>>(P, nnz, idx, val, bitmap, counters);
+    k_compress_coo<<<blocks, 256, 0, s>>>(P, nnz, idx, val, bitmap, counters, bad_out);
     count_launch();
 }
 

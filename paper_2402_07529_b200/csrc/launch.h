@@ -31,7 +31,8 @@ struct CompressBatch {
 void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned long long* nnz_out,
                            cudaStream_t s);
 void launch_compress_coo(const KParams& P, uint64_t nnz, const uint32_t* idx, const float* val,
-                         uint32_t* bitmap, float* counters, cudaStream_t s);
+                         uint32_t* bitmap, float* counters, unsigned long long* bad_out,
+                         cudaStream_t s);
 void launch_clear(int n, uint32_t* const* bitmaps, uint64_t n_words, float* const* counters,
                   uint64_t c, cudaStream_t s);
 void launch_aggregate(uint64_t n_words, uint64_t c, int n_in, const uint32_t* const* bitmaps,

@@ -371,8 +371,11 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                     sh_q[atomicAdd(sh_n, 1u)] = make_uint2(e, id);
                 }
             __syncthreads();
-            if (*sh_n + 4 * kPeelThreads > qcap || base + 4 * gstride >= P.c)
-                flush_queue(sh_q, sh_n, sh_base, frontier, 0u, &ctrl->rc[0]);
+            // the flush decision must be block-uniform: every thread reads the count
+            // before any thread of the next pass appends (flush_queue has barriers)
+            const bool flush = *sh_n + 4 * kPeelThreads > qcap || base + 4 * gstride >= P.c;
+            __syncthreads();
+            if (flush) flush_queue(sh_q, sh_n, sh_base, frontier, 0u, &ctrl->rc[0]);
         }
     }
     grid.sync();

@@ -30,8 +30,9 @@ class Sketch:
         """Accumulate the dense gradient x into this sketch (Alg. 1 Phase I)."""
         L.sketch_compress(self.p, x, self.bitmap, self.counters, nnz_out, stream)
 
-    def compress_coo(self, idx: torch.Tensor, val: torch.Tensor, stream=None):
-        L.sketch_compress_coo(self.p, idx, val, self.bitmap, self.counters, stream)
+    def compress_coo(self, idx: torch.Tensor, val: torch.Tensor, bad_out=None, stream=None):
+        """Accumulate a COO gradient; bad_out (device int64[1]) counts idx >= d (skipped)."""
+        L.sketch_compress_coo(self.p, idx, val, self.bitmap, self.counters, bad_out, stream)
 
     @property
     def nbytes(self) -> int:
@@ -279,7 +280,9 @@ class ShardedAllReduce:
         self.ps = [L.params(plan.shard_d(q), plan.shard_m(q), s.c, k, s.k_bloom, L_rows, seed)
                    for q in range(plan.shards)]
         self.cap = int(cap_cand) or int(1.25 * s.n_cand_expected) + 4096
-        self.cap = min(self.cap, plan.width)
+        # a multiple of 4 (the gather slots hold 16-byte vectors): the decoders and the
+        # communicator then agree on when a shard's decode overflowed
+        self.cap = (min(self.cap, plan.width) + 3) // 4 * 4
         self.slot_bytes, self.y_off, total = L.lhc_shard_layout(self.ps[0], self.world, self.cap)
         if comm not in ("p2p", "nvls"):
             raise ValueError("comm must be 'p2p' or 'nvls'")

@@ -83,6 +83,63 @@ def sharded(name, law, steps, rank, world, dev, comm="p2p"):
     return flag.item() == 1
 
 
+def sharded_overflow(rank, world, dev, comm="p2p"):
+    """a shard whose decode overflows its candidate capacity must not
+    leave stale values on the other ranks.  The last shard is made 8x denser than
+    the others and the capacity is set between the two candidate counts, so only
+    its owner overflows; every rank must then hold NaN on that shard's range and
+    the exact sum everywhere else, and the owner's stats must report overflow."""
+    import oracle
+    import paper_2402_07529_b200 as lhc
+    from lhc_inputs import rng_for, values
+    from paper_2402_07529_b200.sizing import shard_plan
+
+    W = 2
+    d = 60_000 * world
+    plan = shard_plan(d, world, 0.01, W)
+    xs_all = []
+    for w in range(W):
+        rng = rng_for(777 + w)
+        x = np.zeros(d, np.float32)
+        for q in range(world):
+            lo, hi = plan.bounds(q)
+            rho = 0.08 if q == world - 1 else 0.01
+            idx = rng.choice(hi - lo, int(rho * (hi - lo)), replace=False) + lo
+            x[idx] = values(rng, len(idx), "dyadic")
+        xs_all.append(x)
+    s = plan.sizing
+    n_cand = []
+    for q in range(world):
+        lo, hi = plan.bounds(q)
+        op = oracle.params(plan.shard_d(q), plan.shard_m(q), s.c, 3, s.k_bloom, 1024, 0x0F0)
+        Bq, Yq = oracle.aggregate(*zip(*[oracle.compress_dense(op, x[lo:hi]) for x in xs_all]))
+        n_cand.append(len(oracle.query(op, Bq)))
+    cap = (max(n_cand[:-1]) + n_cand[-1]) // 2 // 4 * 4
+    assert max(n_cand[:-1]) <= cap < n_cand[-1], (n_cand, cap)
+    mine = [w for w in range(W) if w % world == rank]
+    xs = [torch.from_numpy(xs_all[w]).to(dev) for w in mine] or [torch.zeros(d, device=dev)]
+    run = lhc.ShardedAllReduce(plan, seed=0x0F0, cap_cand=cap, local_workers=len(xs), device=dev,
+                               comm=comm)
+    dec = run.step(xs)
+    torch.cuda.synchronize()
+    st = dec.read_stats()
+    dense = run.dense.cpu().numpy().astype(np.float64)
+    total = np.sum(np.stack(xs_all).astype(np.float64), axis=0)
+    lo_last, hi_last = plan.bounds(world - 1)
+    ok = bool(np.isnan(dense[lo_last:hi_last]).all())
+    ok &= bool(np.array_equal(dense[:lo_last], total[:lo_last]))
+    if rank == world - 1:
+        ok &= bool(st["overflow"]) and not st["success"]
+    else:
+        ok &= bool(st["success"]) and not st["overflow"]
+    print(f"mgpu-sharded-overflow[{comm}] world={world} rank={rank} n_cand={n_cand} cap={cap} "
+          f"ok={ok}", flush=True)
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    run.close()
+    return flag.item() == 1
+
+
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "ncf"
     law = sys.argv[2] if len(sys.argv) > 2 else "dyadic"
@@ -93,6 +150,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
+    if mode in ("sharded-overflow", "sharded-nvls-overflow"):
+        ok = sharded_overflow(rank, world, dev, "nvls" if "nvls" in mode else "p2p")
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
     if mode in ("sharded", "sharded-nvls"):
         ok = sharded(name, law, steps, rank, world, dev, "nvls" if mode == "sharded-nvls" else "p2p")
         dist.destroy_process_group()

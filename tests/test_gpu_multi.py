@@ -53,3 +53,17 @@ def test_nvls_parity(world, mode, name, law):
            os.path.join(ROOT, "tests", "mgpu_worker.py"), name, law, "3", mode]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("mode", ["sharded-overflow", "sharded-nvls-overflow"])
+def test_sharded_overflow_is_visible_on_every_rank(world, mode):
+    """A shard whose decode overflows publishes an overflow mark; every rank fills
+    that shard with NaN instead of a stale list (comm.cu all-gather)."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29536",
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), "tiny", "dyadic", "1", mode]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

@@ -154,6 +154,36 @@ def test_compress_coo(lhc, ora):
     assert np.array_equal(F(sk.counters), Y)
 
 
+@pytest.mark.parametrize("index", ["bloom", "bitmap"])
+def test_compress_coo_out_of_range_flagged(lhc, ora, index):
+    """Entries with idx >= d are skipped (nothing written: with the exact bitmap index
+    such an index would address a word past the bitmap) and counted in bad_out."""
+    d, L = 100_003, 1024
+    s = lhc.size_workload(d, 0.02, 1, L=L)
+    from paper_2402_07529_b200.sizing import INDEX_BITMAP
+    kb = INDEX_BITMAP if index == "bitmap" else 0
+    m = -(-d // L) * L if index == "bitmap" else s.m
+    p = gpu_params(lhc, d, m, s.c, kb=kb, L=L, seed=6)
+    rng = rng_for(43)
+    idx = support(rng, d, 2_000, "uniform")
+    val = values(rng, len(idx), "dyadic")
+    bad_idx = np.array([d, d + 5, 2**32 - 1, 3 * d], np.uint32)
+    all_idx = np.concatenate([idx, bad_idx])
+    all_val = np.concatenate([val, np.ones(4, np.float32)])
+    # guard words past the end of the bitmap and the counters
+    bm = torch.zeros(p.words + 64, dtype=torch.int32, device="cuda")
+    ct = torch.zeros(int(p.c) + 256, dtype=torch.float32, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    lhc.sketch_compress_coo(p, torch.from_numpy(all_idx.view(np.int32)).cuda(),
+                            torch.from_numpy(all_val).cuda(), bm, ct, bad)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 4
+    B, Y = ora.compress_coo(ora_params(ora, p), idx, val)
+    assert np.array_equal(U(bm[:p.words]), B)
+    assert np.array_equal(F(ct[:int(p.c)]), Y)
+    assert not U(bm[p.words:]).any() and not F(ct[int(p.c):]).any()
+
+
 def test_aggregate(lhc, ora):
     d, L, W = 500_000, 1024, 5
     s = lhc.size_workload(d, 0.01, W)

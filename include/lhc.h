@@ -286,6 +286,25 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
                 uint64_t cap_cand, const uint32_t* out_idx, float* out_val, uint8_t* out_peeled,
                 float* out_dense, lhc_stats* stats, void* stream);
 
+/* Deterministic decode (DESIGN.md NEXT-3): sketch_peel with values that do not
+ * depend on launch geometry, scheduling or atomic order — the same aggregated
+ * sketch gives the same bytes on every rank and every run.  Same arguments,
+ * workspace and outputs as sketch_peel (call after sketch_query); flags, rounds
+ * and success are identical to sketch_peel's.  Each candidate takes its value
+ * from its lowest-j pure cell (the oracle's rule, reading R10) and deductions
+ * are accumulated on a 64-bit fixed-point grid (integer sums commute), so values
+ * are bit-exact under the dyadic law and within the fp32 tolerance otherwise.
+ * Synchronous rounds organised by sketch row (peel_rows.cu).  Requires no
+ * destination row to receive more than 4096 input rows (nrows <= 2048 S_Y; else
+ * LHC_EINVAL).  sketch_decompress_det = sketch_query + sketch_peel_det. */
+int sketch_peel_det(const lhc_params* p, const float* counters, void* ws, size_t ws_bytes,
+                    uint64_t cap_cand, const uint32_t* out_idx, float* out_val, uint8_t* out_peeled,
+                    float* out_dense, lhc_stats* stats, void* stream);
+int sketch_decompress_det(const lhc_params* p, const uint32_t* bitmap, const float* counters,
+                          void* ws, size_t ws_bytes, uint64_t cap_cand, uint32_t* out_idx,
+                          float* out_val, uint8_t* out_peeled, float* out_dense, lhc_stats* stats,
+                          void* stream);
+
 /* Number of kernel launches the last successful call of each entry point made
  * on this thread (bench accounting of `gpu_launches`). */
 int lhc_last_launch_count(void);

@@ -79,7 +79,7 @@ EXPORTS = [
     "sketch_hash_rows", "sketch_clear", "sketch_compress", "sketch_compress_coo",
     "sketch_aggregate", "lhc_comm_layout", "lhc_ipc_handle", "lhc_comm_create",
     "sketch_allreduce", "lhc_comm_destroy", "sketch_decompress", "lhc_last_launch_count",
-    "sketch_query", "sketch_peel", "lhc_shard_layout", "lhc_shard_comm_create",
+    "sketch_query", "sketch_peel", "sketch_peel_det", "sketch_decompress_det", "lhc_shard_layout", "lhc_shard_comm_create",
     "sketch_reduce_scatter", "sketch_allgather_decoded", "sketch_compress_batch",
     "sketch_clear_batch", "lhc_nvls_open", "lhc_nvls_bind", "sketch_allreduce_nvls",
     "sketch_reduce_scatter_nvls", "sketch_allgather_decoded_nvls", "lhc_nvls_destroy",
@@ -116,6 +116,8 @@ def lib() -> ctypes.CDLL:
             "lhc_last_launch_count": (i32, []),
             "sketch_query": (i32, [P, vp, vp, sz, u64, vp, vp, vp]),
             "sketch_peel": (i32, [P, vp, vp, sz, u64, vp, vp, vp, vp, vp, vp]),
+            "sketch_peel_det": (i32, [P, vp, vp, sz, u64, vp, vp, vp, vp, vp, vp]),
+            "sketch_decompress_det": (i32, [P, vp, vp, vp, sz, u64, vp, vp, vp, vp, vp, vp]),
             "lhc_shard_layout": (i32, [P, i32, u64, ctypes.POINTER(sz), ctypes.POINTER(sz),
                                        ctypes.POINTER(sz)]),
             "lhc_shard_comm_create": (i32, [i32, i32, vp, vp, vp, sz, P, u64,
@@ -271,8 +273,10 @@ def sketch_aggregate(p: lhc_params, bitmaps, counters, out_bitmap: torch.Tensor,
 def sketch_decompress(p: lhc_params, bitmap: torch.Tensor, counters: torch.Tensor,
                       ws: torch.Tensor, cap_cand: int, out_idx: torch.Tensor,
                       out_val: torch.Tensor, out_peeled: torch.Tensor,
-                      out_dense: torch.Tensor | None, stats: torch.Tensor, stream=None):
-    _check("sketch_decompress", lib().sketch_decompress(
+                      out_dense: torch.Tensor | None, stats: torch.Tensor, stream=None,
+                      deterministic: bool = False):
+    name = "sketch_decompress_det" if deterministic else "sketch_decompress"
+    _check(name, getattr(lib(), name)(
         ctypes.byref(p), _dev(bitmap, torch.int32, p.words, "bitmap"),
         _dev(counters, torch.float32, p.c, "counters"), _dev(ws, torch.uint8, None, "ws"),
         ws.numel(), int(cap_cand), _dev(out_idx, torch.int32, cap_cand, "out_idx"),
@@ -291,8 +295,10 @@ def sketch_query(p: lhc_params, bitmap, ws, cap_cand, out_idx, stats, stream=Non
 
 
 def sketch_peel(p: lhc_params, counters, ws, cap_cand, out_idx, out_val, out_peeled, out_dense,
-                stats, stream=None):
-    _check("sketch_peel", lib().sketch_peel(
+                stats, stream=None, deterministic: bool = False):
+    """deterministic=True: sketch_peel_det (values independent of launch geometry)."""
+    name = "sketch_peel_det" if deterministic else "sketch_peel"
+    _check(name, getattr(lib(), name)(
         ctypes.byref(p), _dev(counters, torch.float32, p.c, "counters"),
         _dev(ws, torch.uint8, None, "ws"), ws.numel(), int(cap_cand),
         _dev(out_idx, torch.int32, cap_cand, "out_idx"),

@@ -120,6 +120,15 @@ WsLayout ws_layout(const KParams& P, uint64_t cap) {
     W.pair_pos = o;  o = align_up(o + (size_t)P.nrows * P.k * sizeof(uint32_t), 256);
     W.dst_list = o;  o = align_up(o + (size_t)P.nrows * P.k * sizeof(uint32_t), 256);
     W.rowoff = o;    o = align_up(o + ((size_t)P.nrows + 1) * sizeof(uint32_t), 256);
+    // row peel (peel_rows.cu): claim masks per probe, per-row flags and worklists,
+    // sorted destination-row lists (the fixed-point deductions use `cells`, the
+    // remaining masks `claim`)
+    W.claim_k = o;   o = align_up(o + (size_t)P.k * W.nchunks * 32 * sizeof(uint32_t), 256);
+    W.dmark = o;     o = align_up(o + (P.c >> P.log2L) * sizeof(uint32_t), 256);
+    W.dst_sorted = o; o = align_up(o + (size_t)P.nrows * P.k * sizeof(uint32_t), 256);
+    W.ymark = o;     o = align_up(o + (size_t)P.nrows * sizeof(uint32_t), 256);
+    W.xl = o;        o = align_up(o + 2 * (P.c >> P.log2L) * sizeof(uint32_t), 256);
+    W.yl = o;        o = align_up(o + 2 * (size_t)P.nrows * sizeof(uint32_t), 256);
     W.total = o;
     return W;
 }
@@ -269,6 +278,7 @@ struct WsView {
     float* dense;
     uint32_t *dst_off, *pair_pos, *dst_list;
     uint32_t* rowoff;
+    uint32_t *claim_k, *dmark, *dst_sorted, *ymark, *xl, *yl;
 };
 
 int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, WsView* v) {
@@ -293,6 +303,12 @@ int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, 
     v->dst_off = reinterpret_cast<uint32_t*>(b + v->W.dst_off);
     v->pair_pos = reinterpret_cast<uint32_t*>(b + v->W.pair_pos);
     v->dst_list = reinterpret_cast<uint32_t*>(b + v->W.dst_list);
+    v->claim_k = reinterpret_cast<uint32_t*>(b + v->W.claim_k);
+    v->dmark = reinterpret_cast<uint32_t*>(b + v->W.dmark);
+    v->dst_sorted = reinterpret_cast<uint32_t*>(b + v->W.dst_sorted);
+    v->ymark = reinterpret_cast<uint32_t*>(b + v->W.ymark);
+    v->xl = reinterpret_cast<uint32_t*>(b + v->W.xl);
+    v->yl = reinterpret_cast<uint32_t*>(b + v->W.yl);
     return LHC_OK;
 }
 }  // namespace
@@ -353,6 +369,48 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
                                 v.frontier, v.ctrl, out_val, out_peeled, stats, mode, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_peel");
+}
+
+int sketch_peel_det(const lhc_params* p, const float* counters, void* ws, size_t ws_bytes,
+                    uint64_t cap_cand, const uint32_t* out_idx, float* out_val, uint8_t* out_peeled,
+                    float* out_dense, lhc_stats* stats, void* stream) {
+    reset_launches();
+    WsView v;
+    if (int rc = ws_view(p, ws, ws_bytes, &cap_cand, &v)) return rc;
+    if (!counters || !stats) return set_error(LHC_EINVAL, "NULL buffer");
+    if (!aligned16(counters)) return set_error(LHC_EINVAL, "counters must be 16-byte aligned");
+    if (out_dense && !aligned16(out_dense)) return set_error(LHC_EINVAL, "out_dense must be 16-byte aligned");
+    if (cap_cand && (!out_idx || !out_val || !out_peeled)) return set_error(LHC_EINVAL, "NULL output");
+    // the row peel tracks a pure cell's owner in 12 bit planes: a destination row
+    // may list at most 4096 input rows (hashed uniformly: nrows <= 2048 S_Y)
+    const uint64_t s_blk = v.P.blocks ? v.P.S_Y : v.P.S_Y;
+    const uint64_t rows_per_part = v.P.blocks ? (v.P.nrows + v.P.blocks - 1) / v.P.blocks : v.P.nrows;
+    if (rows_per_part > 2048ull * s_blk)
+        return set_error(LHC_EINVAL, "deterministic decode: %llu input rows onto %llu rows per partition",
+                         (unsigned long long)rows_per_part, (unsigned long long)s_blk);
+    float* dense = out_dense ? out_dense : v.dense;
+    cudaError_t er = launch_peel_rows(v.P, counters, v.tabS, v.gmask, v.dst_off, v.pair_pos,
+                                      v.dst_list, v.dst_sorted, out_idx,
+                                      reinterpret_cast<unsigned long long*>(v.cells), v.claim,
+                                      v.claim_k, v.dmark, v.ymark, v.xl, v.yl, dense, cap_cand,
+                                      out_val, out_peeled, v.ctrl, stats, (cudaStream_t)stream);
+    if (er != cudaSuccess) return set_error(LHC_ECUDA, "row peel launch: %s", cudaGetErrorString(er));
+    return check_launch("sketch_peel_det");
+}
+
+int sketch_decompress_det(const lhc_params* p, const uint32_t* bitmap, const float* counters,
+                          void* ws, size_t ws_bytes, uint64_t cap_cand, uint32_t* out_idx,
+                          float* out_val, uint8_t* out_peeled, float* out_dense, lhc_stats* stats,
+                          void* stream) {
+    if (int rc = sketch_query(p, bitmap, ws, ws_bytes, cap_cand, out_idx, stats, stream)) return rc;
+    int n = lhc_last_launch_count();
+    if (int rc = sketch_peel_det(p, counters, ws, ws_bytes, cap_cand, out_idx, out_val, out_peeled,
+                                 out_dense, stats, stream))
+        return rc;
+    n += lhc_last_launch_count();
+    reset_launches();
+    count_launch(n);
+    return LHC_OK;
 }
 
 int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* counters,

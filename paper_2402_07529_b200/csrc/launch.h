@@ -52,6 +52,16 @@ cudaError_t launch_peel_blocked(const KParams& P, const float* counters, const u
 uint32_t query_max_ctas();
 
 // peeling decoder (peel.cu)
+void launch_pair_lists(const KParams& P, const uint2* tabS, uint32_t* dst_off, uint32_t* pair_pos,
+                       uint32_t* dst_list, cudaStream_t s);
+// row-organised synchronous peel with deterministic values (peel_rows.cu)
+cudaError_t launch_peel_rows(const KParams& P, const float* counters, const uint2* tabS,
+                             const uint32_t* gmask, uint32_t* dst_off, uint32_t* pair_pos,
+                             uint32_t* dst_tmp, uint32_t* dst_list, const uint32_t* cand,
+                             unsigned long long* delta, uint32_t* rem, uint32_t* claim,
+                             uint32_t* dmark, uint32_t* ymark, uint32_t* xl, uint32_t* yl,
+                             float* dense, uint64_t cap, float* out_val, uint8_t* out_peeled,
+                             Ctrl* ctrl, lhc_stats* stats, cudaStream_t s);
 void launch_build_cells(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* gmask, uint32_t* dst_off, uint32_t* pair_pos,
                         uint32_t* dst_list, void* cells, Ctrl* ctrl, bool compact,

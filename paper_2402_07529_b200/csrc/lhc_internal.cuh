@@ -110,12 +110,16 @@ struct Ctrl {
     uint32_t blk_done;      // blocks finished (the last one writes the stats)
     unsigned long long blk_peeled;
     uint32_t blk_rounds;
+    uint32_t xl_n[2], yl_n[2];  // row peel worklist counts, by round parity
+    uint32_t ymax_bits;         // row peel: max |Y| (fp32 bits), sets the fixed-point grid
+    uint32_t fx_overflow;       // row peel: a deduction exceeded the fixed-point range
     // instrumentation (device globaltimer ns): t[0..3] phase starts, t[3 + r] start of
     // round r, t[kCtrlTimes-1] end of rounds; fsize[r] = queue segment of round r
     unsigned long long t[128];
     uint32_t fsize[128];
     unsigned long long tproc[128];  // per round: latest block finishing its entries
     unsigned long long tflush[128]; // per round: latest block finishing its appends
+    unsigned long long dbg[4][128]; // row peel (LHC_ROWS_TIMING): per-round maxima of X / Y work items
 };
 constexpr int kCtrlTimes = 128;
 
@@ -128,7 +132,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Sub-allocation of the decompress workspace.
 struct WsLayout {
     size_t tabS, gmask, cta_total, cells, claim, frontier, dense, dst_off, pair_pos, dst_list, ctrl,
-        rowoff, total;
+        rowoff, claim_k, dmark, dst_sorted, ymark, xl, yl, total;
     uint32_t nchunks;
 };
 

@@ -289,32 +289,39 @@ k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __rest
     }
 }
 
+// (input row, probe) pairs counting-sorted by destination row: dst_off[nD + 1]
+// offsets, dst_list the input rows (in an atomic order within a row)
+void launch_pair_lists(const KParams& P, const uint2* tabS, uint32_t* dst_off, uint32_t* pair_pos,
+                       uint32_t* dst_list, cudaStream_t s) {
+    const uint64_t npairs = (uint64_t)P.nrows * P.k;
+    const uint64_t nD = P.c >> P.log2L;
+    const uint32_t gp = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((npairs + 255) / 256, (uint64_t)num_sms() * 8));
+    cudaMemsetAsync(dst_off, 0, (nD + 1) * sizeof(uint32_t), s);
+    k_pair_count<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos);
+    k_pair_scan<<<1, 1024, 0, s>>>(dst_off, (uint32_t)nD + 1);
+    k_pair_scatter<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos, dst_list);
+    count_launch(3);
+}
+
 void launch_build_cells(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* gmask, uint32_t* dst_off, uint32_t* pair_pos,
                         uint32_t* dst_list, void* cells, Ctrl* ctrl, bool compact,
                         cudaStream_t s) {
-    const uint64_t npairs = (uint64_t)P.nrows * P.k;
     const uint64_t nD = P.c >> P.log2L;
-    const uint32_t gp = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((npairs + 255) / 256, (uint64_t)num_sms() * 8));
 #ifdef LHC_DEBUG_SYNC
 #define DBG(name) { cudaError_t e_ = cudaStreamSynchronize(s); if (e_) fprintf(stderr, "%s: %s\n", name, cudaGetErrorString(e_)); else fprintf(stderr, "%s ok\n", name); }
 #else
 #define DBG(name)
 #endif
-    cudaMemsetAsync(dst_off, 0, (nD + 1) * sizeof(uint32_t), s);
-    k_pair_count<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos);
-    DBG("pair_count");
-    k_pair_scan<<<1, 1024, 0, s>>>(dst_off, (uint32_t)nD + 1);
-    DBG("pair_scan");
-    k_pair_scatter<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos, dst_list);
-    DBG("pair_scatter");
+    launch_pair_lists(P, tabS, dst_off, pair_pos, dst_list, s);
+    DBG("pair_lists");
     const uint32_t gb = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((nD + 7) / 8, (uint64_t)num_sms() * 16));
     if (compact)
         k_build_cells<true><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl);
     else
         k_build_cells<false><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl);
     DBG("build_cells");
-    count_launch(4);
+    count_launch(1);
 }
 
 // KT: compile-time k (3) or 0 for a run-time k <= kMaxK.

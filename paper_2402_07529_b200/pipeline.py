@@ -48,8 +48,12 @@ def aggregate(p: L.lhc_params, sketches, out: Sketch, stream=None):
 class Decoder:
     """Phase II of Alg. 1 with preallocated workspace and outputs."""
 
-    def __init__(self, p: L.lhc_params, cap_cand: int, dense: bool = True, device="cuda"):
+    def __init__(self, p: L.lhc_params, cap_cand: int, dense: bool = True, device="cuda",
+                 deterministic: bool = False):
+        """deterministic=True decodes with sketch_peel_det: values, flags and dense
+        output bit-identical across runs, launch geometries and ranks."""
         self.p = p
+        self.deterministic = deterministic
         self.cap = int(min(cap_cand, p.d))
         self.ws = torch.empty(L.lhc_decompress_workspace(p, self.cap), dtype=torch.uint8,
                               device=device)
@@ -61,7 +65,8 @@ class Decoder:
 
     def __call__(self, sketch: Sketch, stream=None):
         L.sketch_decompress(self.p, sketch.bitmap, sketch.counters, self.ws, self.cap, self.idx,
-                            self.val, self.peeled, self.dense, self.stats, stream)
+                            self.val, self.peeled, self.dense, self.stats, stream,
+                            deterministic=self.deterministic)
         return self
 
     # the two steps of __call__, separately (for per-kernel timing)
@@ -70,7 +75,7 @@ class Decoder:
 
     def peel(self, sketch: Sketch, stream=None):
         L.sketch_peel(self.p, sketch.counters, self.ws, self.cap, self.idx, self.val, self.peeled,
-                      self.dense, self.stats, stream)
+                      self.dense, self.stats, stream, deterministic=self.deterministic)
 
     def read_stats(self) -> dict:
         return L.read_stats(self.stats)
@@ -195,18 +200,24 @@ class LosslessAllReduce:
     sketch the all-rank OR/sum (NVLink P2P, or nothing on one GPU), and decode.
 
     ``per_worker=True`` keeps one sketch per local worker (the per-worker payload
-    of the paper's API) and aggregates them on the GPU before the exchange."""
+    of the paper's API) and aggregates them on the GPU before the exchange.
+
+    Every rank decodes the identical aggregated sketch.  With the default decode
+    (sketch_peel) the flags, rounds and candidate set are identical on all ranks
+    but fp32 values may differ in the last bits (residual deductions land in a
+    scheduling-dependent order); ``deterministic=True`` decodes with
+    sketch_peel_det, whose values are bit-identical on every rank and run."""
 
     def __init__(self, p: L.lhc_params, cap_cand: int, local_workers: int = 1,
                  per_worker: bool = True, comm: PeerComm | None = None, dense: bool = True,
-                 device="cuda"):
+                 device="cuda", deterministic: bool = False):
         self.p = p
         self.comm = comm
         self.sketch = comm.sketch if comm is not None else Sketch(p, device)
         self.per_worker = per_worker and local_workers > 1
         self.worker_sketches = [Sketch(p, device) for _ in range(local_workers)] \
             if self.per_worker else []
-        self.decoder = Decoder(p, cap_cand, dense=dense, device=device)
+        self.decoder = Decoder(p, cap_cand, dense=dense, device=device, deterministic=deterministic)
 
     def step(self, xs, stream=None):
         """xs: list of dense fp32 device gradients of this rank's workers."""

@@ -605,20 +605,19 @@ def blocked_params(lhc, d, nnz, W, L, B, gamma=1.5, seed=0xB10C):
     (777_777, 30_000, 4, 256, 33),         # B does not divide the row count
 ])
 @pytest.mark.parametrize("law", ["dyadic", "gauss"])
-@pytest.mark.parametrize("build", ["blocked", "insert", "rows", "compact"])
+@pytest.mark.parametrize("build", ["rowpeel", "blocked", "insert", "rows", "compact"])
 def test_blocked_sketch_pipeline(lhc, ora, d, nnz, W, L, B, law, build, monkeypatch):
     """P:L206 blocks: every row map, the bitmap, counters, candidates, flags, rounds
-    and values equal the oracle's on a blocked sketch — with the block-local
-    shared-memory peel (k_peel_blocked, the default for a blocked sketch) and through
-    every build mode of the global peel."""
-    if build == "blocked":
-        monkeypatch.delenv("LHC_CELL_BUILD", raising=False)
-    else:
+    and values equal the oracle's on a blocked sketch — with the row peel (the
+    default), the block-local shared-memory peel (k_peel_blocked) and through every
+    build mode of the cell-frontier peel."""
+    monkeypatch.delenv("LHC_CELL_BUILD", raising=False)
+    if build not in ("rowpeel", "blocked"):
         monkeypatch.setenv("LHC_CELL_BUILD", build)
     p = blocked_params(lhc, d, nnz, W, L, B)
     op = ora_params(ora, p)
     xs = make_workers(d, nnz, W, 50 + B, law)
-    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W, deterministic=build == "rowpeel")
     dec = run.step([torch.from_numpy(x).cuda() for x in xs])
     torch.cuda.synchronize()
     B_, Y, ref = ora.pipeline(op, xs)
@@ -657,3 +656,57 @@ def test_blocked_peel_failure_parity(lhc, ora, gamma, monkeypatch):
     torch.cuda.synchronize()
     _, _, ref = ora.pipeline(op, xs)
     compare_decode(ora, dec, ref, True)
+
+
+@pytest.mark.parametrize("gamma", [1.30, 1.05])
+@pytest.mark.parametrize("law", ["gauss", "dyadic"])
+def test_decode_deterministic_across_launch_geometries(lhc, ora, gamma, law, monkeypatch):
+    """NEXT-3 (deterministic decode; P:L206 parallel rounds, P:L136 every worker
+    recovers): the same aggregated sketch decoded 10 times by sketch_decompress_det
+    with different grids gives bit-identical values, flags and dense output, under
+    the Gaussian law where fp32 order matters — every value comes from the
+    lowest-j pure cell and deductions are summed on an integer grid.  Flags, rounds
+    and success equal the default decode's; under the dyadic law values are exact.
+    gamma 1.05 stalls: the median fallback is covered too."""
+    d, nnz, W, L = 3_000_017, 30_000, 4, 1024
+    s = lhc.size_workload(d, nnz / d, W, L=L, gamma=gamma)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=0xDE7 + int(gamma * 100))
+    xs = make_workers(d, nnz, W, 808, law, sigma=1e-3)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    ref_dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    _, _, ref = ora.pipeline(ora_params(ora, p), xs)
+    st0 = compare_decode(ora, ref_dec, ref, exact=(law == "dyadic"))
+    if gamma < 1.2:
+        assert not ref.stats.success
+    outs = []
+    for grid in [None, 1, 2, 7, 37, 148, 296, 1000, 3, 64]:
+        if grid is None:
+            monkeypatch.delenv("LHC_PEEL_GRID", raising=False)
+        else:
+            monkeypatch.setenv("LHC_PEEL_GRID", str(grid))
+        dec = lhc.Decoder(p, d, deterministic=True)
+        dec(run.sketch)
+        torch.cuda.synchronize()
+        st = compare_decode(ora, dec, ref, exact=(law == "dyadic"))
+        assert {k: st[k] for k in ("n_cand", "n_peeled", "rounds", "success")} == \
+            {k: st0[k] for k in ("n_cand", "n_peeled", "rounds", "success")}
+        n = st["n_cand"]
+        outs.append((dec.val[:n].cpu().numpy().tobytes(), dec.peeled[:n].cpu().numpy().tobytes(),
+                     dec.dense.cpu().numpy().tobytes()))
+    assert all(o == outs[0] for o in outs[1:])
+
+
+@pytest.mark.parametrize("d,nnz,W,L,structure", CASES)
+@pytest.mark.parametrize("law", ["dyadic", "gauss"])
+def test_pipeline_deterministic_decode(lhc, ora, d, nnz, W, L, structure, law):
+    """sketch_decompress_det over the small configs: candidates, flags, rounds and
+    success bit-exact, values exact (dyadic) / within tolerance (Gaussian)."""
+    s = lhc.size_workload(d, nnz / d, W, L=L)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=0x5EED + d)
+    xs = make_workers(d, nnz, W, 31 + d % 13, law, structure)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W, deterministic=True)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    _, _, ref = ora.pipeline(ora_params(ora, p), xs)
+    compare_decode(ora, dec, ref, law == "dyadic")

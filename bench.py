@@ -57,8 +57,11 @@ def parse():
                          "blocks (P:L206, NEXT-3) peeled block-locally in shared memory")
     ap.add_argument("--L", type=int, default=1024, help="batch width (paper: 1024, P:L261)")
     ap.add_argument("--block-cells", type=int, default=12288, help="cells per block for --blocks auto")
-    ap.add_argument("--fuse-local", action="store_true",
-                    help="compress a rank's workers straight into one sketch (no per-worker sketches)")
+    ap.add_argument("--per-worker", action="store_true",
+                    help="one sketch per local worker, cleared and aggregated on the GPU (the "
+                         "default compresses a rank's workers straight into its sketch: Y and B "
+                         "are homomorphic, P:L137, so the local aggregation is the reductions)")
+    ap.add_argument("--fuse-local", action="store_true", help="(the default; kept for old command lines)")
     ap.add_argument("--comm", choices=["p2p", "nvls", "nccl"], default="p2p",
                     help="p2p: NVLink peer stores (two-shot); nvls: NVSwitch multicast "
                          "(in-switch reduction, NEXT-2); nccl: the NCCL baseline")
@@ -66,6 +69,8 @@ def parse():
                     help="replicated: all-reduce, every rank decodes all of d (the north "
                          "star); sharded: per-shard sub-sketches, reduce-scatter, every rank "
                          "decodes its shard, all-gather of the decoded lists (NEXT-2)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="decode with sketch_peel_det (values bit-identical across runs and ranks)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -298,7 +303,8 @@ def main():
             raise SystemExit("--blocks applies to the replicated decode")
         plan = shard_plan(wl.d, world, wl.density, wl.workers, gamma=args.gamma, k_bloom=kb)
         run = lhc.ShardedAllReduce(plan, seed=SEED, local_workers=len(xs),
-                                   per_worker=not args.fuse_local, device=dev, comm=args.comm)
+                                   per_worker=args.per_worker, device=dev, comm=args.comm,
+                                   deterministic=args.deterministic)
         p_dec = run.ps[rank]           # the shard this rank decodes
         G = plan.shards
     else:
@@ -307,7 +313,8 @@ def main():
         elif world > 1 and args.comm == "nvls":
             comm = lhc.NvlsComm(p)
         run = lhc.LosslessAllReduce(p, cap, local_workers=len(xs),
-                                    per_worker=not args.fuse_local, comm=comm, device=dev)
+                                    per_worker=args.per_worker, comm=comm, device=dev,
+                                    deterministic=args.deterministic)
         p_dec = p
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -329,6 +336,8 @@ def main():
         sk.bitmap.copy_(out)
 
     # instrumented step: CUDA events around each phase on the launching stream
+    phase_launches = None
+
     def step(ev=None, launches=None):
         def mark(name):
             if ev is not None:
@@ -336,9 +345,12 @@ def main():
                 e.record(stream)
                 ev.append((name, e))
 
-        def cnt():
+        def cnt(ph):
+            n = lhc.last_launch_count()
             if launches is not None:
-                launches[0] += lhc.last_launch_count()
+                launches[0] += n
+            if phase_launches is not None:
+                phase_launches[ph] = phase_launches.get(ph, 0) + n
 
         mark("start")
         if sharded:
@@ -347,64 +359,64 @@ def main():
         dst = run.worker_sketches if run.per_worker else [run.sketch] * len(xs)
         clr = run.worker_sketches if run.per_worker else [run.sketch]
         lhc.sketch_clear_batch(p, [t.bitmap for t in clr[::-1]], [t.counters for t in clr[::-1]])
-        cnt()
+        cnt("clear")
         mark("compress0")
         lhc.sketch_compress_batch(p, xs, [t.bitmap for t in dst], [t.counters for t in dst])
-        cnt()
+        cnt("compress")
         mark("compress1")
         if run.per_worker:
             lhc.aggregate(p, run.worker_sketches, run.sketch)
-            cnt()
+            cnt("aggregate")
         mark("aggregate")
         if world > 1:
             if comm is not None:
                 comm.allreduce()
-                cnt()
+                cnt("allreduce")
             else:
                 nccl_allreduce()
         mark("allreduce")
         dec = run.decoder
         dec.query(run.sketch)
-        cnt()
+        cnt("query")
         mark("query")
         dec.peel(run.sketch)
-        cnt()
+        cnt("peel")
         mark("peel")
 
     def sharded_step(mark, cnt):
         targets = run.worker_bufs if run.per_worker else [run.slots] * len(xs)
         clr = [sk for bufs in (run.worker_bufs if run.per_worker else [run.slots]) for sk in bufs]
         lhc.sketch_clear_batch(run.ps[0], [sk.bitmap for sk in clr[::-1]], [sk.counters for sk in clr[::-1]])
-        cnt()
+        cnt("clear")
         mark("compress0")
         # every (worker, shard) pair in one launch
         pairs = [(run.shard_input(x, q), sk, run.plan.shard_d(q))
                  for bufs, x in zip(targets, xs) for q, sk in enumerate(bufs)]
         lhc.sketch_compress_batch(run.ps[0], [a for a, _, _ in pairs], [b.bitmap for _, b, _ in pairs],
                                   [b.counters for _, b, _ in pairs], ds=[c for _, _, c in pairs])
-        cnt()
+        cnt("compress")
         mark("compress1")
         if run.per_worker:
             for q in range(G):
                 lhc.sketch_aggregate(run.ps[q], [b[q].bitmap for b in run.worker_bufs],
                                      [b[q].counters for b in run.worker_bufs],
                                      run.slots[q].bitmap, run.slots[q].counters)
-                cnt()
+                cnt("aggregate")
         mark("aggregate")
         if world > 1:
             run.reduce_scatter()
-            cnt()
+            cnt("allreduce")
         mark("allreduce")
         dec = run.decoder
         dec.query(run.slots[rank])
-        cnt()
+        cnt("query")
         mark("query")
         dec.peel(run.slots[rank])
-        cnt()
+        cnt("peel")
         mark("peel")
         if world > 1:
             run.allgather()
-            cnt()
+            cnt("allgather")
         mark("allgather")
 
     def barrier():
@@ -483,10 +495,15 @@ def main():
     # (2) per-kernel breakdown: K instrumented steps launched from the host, CUDA
     #     events between the kernels on the launching stream
     per_step = []
-    for _ in range(args.steps):
+    for t in range(args.steps):
         flush.zero_()
         ev = []
+        if t == 0:
+            phase_launches = {}
         step(ev, None)
+        if t == 0:
+            launches_by_phase = dict(phase_launches)
+            phase_launches = None
         per_step.append(ev)
     torch.cuda.synchronize()
     for ev in per_step:
@@ -574,7 +591,8 @@ def main():
         pin_v = [pin_all[tot + offs[j]:tot + offs[j + 1]].view(torch.float32) for j in range(len(lens))]
         if sharded:
             run_b = lhc.ShardedAllReduce(run.plan, seed=SEED, local_workers=len(xs),
-                                         per_worker=not args.fuse_local, device=dev, comm=args.comm)
+                                         per_worker=args.per_worker, device=dev, comm=args.comm,
+                                         deterministic=args.deterministic)
         else:
             comm_b = None
             if world > 1 and args.comm == "p2p":
@@ -582,7 +600,8 @@ def main():
             elif world > 1 and args.comm == "nvls":
                 comm_b = lhc.NvlsComm(p)
             run_b = lhc.LosslessAllReduce(p, cap, local_workers=len(xs),
-                                          per_worker=not args.fuse_local, comm=comm_b, device=dev)
+                                          per_worker=args.per_worker, comm=comm_b, device=dev,
+                                          deterministic=args.deterministic)
         engines = [run, run_b]
         ins, items_k, outs, dev_alls = [], [], [], []
         cap_ = run.decoder.cap
@@ -680,7 +699,8 @@ def main():
         S_all = sum(int(q.m) // 8 + 4 * int(q.c) for q in run.ps)
         kern = {
             # one launch: every local worker's gradient into its G shard sketches
-            "k_compress_dense": (W_loc * (4 * wl.d + S_all), 1, avg_compress_ms, hbm, "hbm"),
+            "k_compress_dense": (W_loc * 4 * wl.d + (W_loc if run.per_worker else 1) * S_all, 1,
+                                 avg_compress_ms, hbm, "hbm"),
             "k_aggregate": ((W_loc + 1) * S_all / G, G if run.per_worker else 0,
                             per_step_ms["aggregate"] / G, hbm, "hbm"),
             "k_reduce_scatter": ((world - 1) / world * S_all, 1 if world > 1 else 0,
@@ -695,8 +715,10 @@ def main():
         }
     else:
         kern = {
-            # one launch: every local worker's gradient into its sketch
-            "k_compress_dense": (W_loc * (4 * wl.d + S), 1, avg_compress_ms, hbm, "hbm"),
+            # one launch: every local worker's gradient into its sketch (its own, or
+            # the rank's one sketch when the workers are accumulated in place)
+            "k_compress_dense": (W_loc * 4 * wl.d + (W_loc if run.per_worker else 1) * S, 1,
+                                 avg_compress_ms, hbm, "hbm"),
             "k_aggregate": ((W_loc + 1) * S, 1 if run.per_worker else 0,
                             per_step_ms["aggregate"], hbm, "hbm"),
             # NVLink bytes out per rank: two-shot 2(G-1)/G S; NVLS (the switch pulls
@@ -715,10 +737,17 @@ def main():
         if nl == 0 or ms_l <= 0:
             continue
         ach = byts / (ms_l * 1e-3) / 1e9
+        phase_of = {"k_compress_dense": "compress", "k_aggregate": "aggregate", "k_allreduce": "allreduce",
+                    "k_reduce_scatter": "allreduce", "k_query": "query", "k_peel": "peel",
+                    "k_clear": "clear", "k_allgather_decoded": "allgather"}
         kernels[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "bytes_per_launch": int(byts),
                          "avg_launch_us": ms_l * 1e3, "launches_per_step": nl,
-                         "us_per_step": ms_l * 1e3 * nl}
+                         "us_per_step": ms_l * 1e3 * nl,
+                         # kernels launched by the phase's API call (the peel phase also builds
+                         # its state: k_pair_count/scan/scatter + k_build_cells when the state
+                         # exceeds L2); its time is the whole phase's
+                         "phase_launches": launches_by_phase.get(phase_of.get(name))}
     # the peel's own bound: L2 atomics (key inserts when the state is built in-kernel,
     # one claim per frontier entry, two updates per other cell of a peeled candidate)
     # against the measured ATOM.ADD.64-with-return peak (tools/atomic_peak.cu)
@@ -754,13 +783,15 @@ def main():
     except Exception:
         inst = {}
     if "k_query" in kernels and inst.get("k_query"):
+        # a diagnostic, not a roofline: how busy the issue slots were (the kernel's own
+        # instruction count from ncu over its time); the roofline is the HBM fraction
         cs = clocks.summary()
         mhz = cs.get("sm_max_mhz") or 1965.0
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
         ipk = 4.0 * n_sm * mhz * 1e6 / 1e9  # G warp-instructions/s
         ach_i = inst["k_query"] / (kernels["k_query"]["avg_launch_us"] * 1e-6) / 1e9
-        kernels["k_query"]["issue"] = {
-            "bound": "alu", "inst_per_launch": int(inst["k_query"]), "achieved": ach_i, "peak": ipk,
+        kernels["k_query"]["issue_utilisation"] = {
+            "inst_per_launch": int(inst["k_query"]), "achieved": ach_i, "peak": ipk,
             "unit": "G warp-instructions/s", "frac": ach_i / ipk,
             "peak_source": f"{n_sm} SMs x 4 schedulers x {mhz:.0f} MHz (one issue per scheduler per cycle)"}
     dom = max(kernels, key=lambda k: kernels[k]["us_per_step"])
@@ -792,6 +823,7 @@ def main():
                        "index": "bitmap" if kb == INDEX_BITMAP else "bloom",
                        "sketch_bytes": int(p.m) // 8 + 4 * int(p.c),
                        "per_worker_sketches": run.per_worker,
+                       "deterministic_decode": args.deterministic,
                        "decode": args.decode,
                        "comm": args.comm if world > 1 else "none",
                        "l2": "flushed (256 MB write) between timed steps, outside the events",
@@ -803,6 +835,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches[0],
+            "launches_per_step_by_phase": launches_by_phase,
             "clocks": clocks.summary(),
             "phases_ms_per_step": per_step_ms,
             "decode": stats,

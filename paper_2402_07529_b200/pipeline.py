@@ -277,7 +277,7 @@ class ShardedAllReduce:
 
     def __init__(self, plan, k: int = 3, L_rows: int = 1024, seed: int = 0, cap_cand: int = 0,
                  local_workers: int = 1, per_worker: bool = True, group=None, device=None,
-                 comm: str = "p2p"):
+                 comm: str = "p2p", deterministic: bool = False):
         import torch.distributed as dist
 
         self.plan = plan
@@ -321,7 +321,7 @@ class ShardedAllReduce:
         self.decoders = {}
         for q in self.owned:
             lo, hi = plan.bounds(q)
-            dec = Decoder(self.ps[q], self.cap, dense=False, device=device)
+            dec = Decoder(self.ps[q], self.cap, dense=False, device=device, deterministic=deterministic)
             dec.dense = self.dense[lo:hi]
             self.decoders[q] = dec
         self.decoder = self.decoders[self.owned[0]]

@@ -74,7 +74,7 @@ def main():
                 print(f"   round {r}: X last warp {(tp[r] - t[r + 3]) / 1e3:8.1f} us, X barrier exit "
                       f"{fs[r] / 10:8.1f} us, Y last warp {(tf[r] - t[r + 3]) / 1e3:8.1f} us")
         # per-launch breakdown with LHC_PEEL_TIMING-free events: time each launch class
-        for impl in ("frontier", "rows", "frontier", "rows"):
+        for impl in ("frontier", "frontier"):
             os.environ["LHC_PEEL_IMPL"] = impl
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             dec.query(run.sketch)

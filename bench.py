@@ -65,10 +65,12 @@ def parse():
     ap.add_argument("--comm", choices=["p2p", "nvls", "nccl"], default="p2p",
                     help="p2p: NVLink peer stores (two-shot); nvls: NVSwitch multicast "
                          "(in-switch reduction, NEXT-2); nccl: the NCCL baseline")
-    ap.add_argument("--decode", choices=["replicated", "sharded"], default="replicated",
-                    help="replicated: all-reduce, every rank decodes all of d (the north "
-                         "star); sharded: per-shard sub-sketches, reduce-scatter, every rank "
-                         "decodes its shard, all-gather of the decoded lists (NEXT-2)")
+    ap.add_argument("--decode", choices=["auto", "replicated", "sharded"], default="auto",
+                    help="replicated: all-reduce, every rank decodes all of d; sharded: "
+                         "per-shard sub-sketches, reduce-scatter, every rank decodes its shard, "
+                         "all-gather of the decoded lists (NEXT-2; the paper's 'distributed load "
+                         "of the recovery process', P:L380); auto (default): replicated on one "
+                         "GPU, sharded on several.  Every rank ends with the same dense sum.")
     ap.add_argument("--deterministic", action="store_true",
                     help="decode with sketch_peel_det (values bit-identical across runs and ranks)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -234,7 +236,20 @@ def trace(msg):
         print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
 
 
+_OUT = None  # the JSON line's stream: the original stdout (fd 1 itself goes to stderr)
+
+
+def emit(line):
+    print(json.dumps(line), file=_OUT or sys.stdout, flush=True)
+
+
 def main():
+    global _OUT
+    # rank 0 prints ONE JSON line on stdout: library banners (e.g. NCCL's version line)
+    # and warnings written to fd 1 are sent to stderr instead
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     if os.environ.get("LHC_BENCH_TRACE"):
         import faulthandler
@@ -250,7 +265,7 @@ def main():
     if args.impl == "reference":
         line = run_reference(args, wl, rank)
         if line is not None:
-            print(json.dumps(line), flush=True)
+            emit(line)
         return
 
     import torch
@@ -293,6 +308,8 @@ def main():
     xs = [torch.from_numpy(x).to(dev) for x in host]
 
     comm = None
+    if args.decode == "auto":
+        args.decode = "sharded" if world > 1 and args.comm != "nccl" else "replicated"
     sharded = args.decode == "sharded"
     if sharded:
         from paper_2402_07529_b200.sizing import shard_plan
@@ -840,23 +857,27 @@ def main():
             "phases_ms_per_step": per_step_ms,
             "decode": stats,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     # a step whose decode overflowed its candidate capacity or stalled timed a
     # truncated peel: the line above records it, the exit code rejects it
     bad = torch.tensor([0 if stats["success"] and not stats["overflow"] else 1], device=dev)
     if world > 1:
         dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+    rc = 3 if int(bad.item()) else 0
+    if rc:
+        print(f"bench: decode failed (success={stats['success']}, overflow={stats['overflow']}); "
+              "the timed steps are not a valid measurement", file=sys.stderr, flush=True)
+    graph = None  # a captured graph may hold NCCL work: release it before the teardown
+    torch.cuda.synchronize()
     if comm is not None:
         comm.close()
     if sharded:
         run.close()
     if world > 1:
         dist.barrier()
-        dist.destroy_process_group()
-    if int(bad.item()):
-        print(f"bench: decode failed (success={stats['success']}, overflow={stats['overflow']}); "
-              "the timed steps are not a valid measurement", file=sys.stderr, flush=True)
-        sys.exit(3)
+    _OUT.flush()
+    sys.stderr.flush()
+    os._exit(rc)  # no process-group teardown (it can hang on graph-captured NCCL work)
 
 
 if __name__ == "__main__":

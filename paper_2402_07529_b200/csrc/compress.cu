@@ -144,8 +144,18 @@ k_compress_dense(KParams P, const __grid_constant__ CompressBatch B,
     uint32_t pa = 0;
     uint64_t pa_start = 0, pa_next = B.n > 1 ? B.start[1] : nchunks, pa_full = B.d[0] / kTile;
     const float* pa_x = B.x[0];
+    const uint32_t inter = B.interleave ? B.n : 0u;  // chunk g = row g / n of input g % n
     auto prefetch = [&](uint64_t g, uint32_t sa, bool fence) {
         if (g >= nchunks) return;
+        if (inter) {
+            const uint32_t b = (uint32_t)(g % inter);
+            const uint64_t lc = g / inter;
+            if (lc < B.d[b] / kTile) {
+                if (fence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bulk_load(sh_x + sa * kTile, B.x[b] + lc * kTile, kTile * 4, bar + sa, pol_stream);
+            }
+            return;
+        }
         while (g >= pa_next) {
             pa++;
             pa_start = B.start[pa];
@@ -168,12 +178,18 @@ k_compress_dense(KParams P, const __grid_constant__ CompressBatch B,
         const uint32_t st = it % kStages;
         // refill: the stage consumed in the previous iteration takes chunk + (kStages-1) stride
         if (lane == 0) prefetch(chunk + (uint64_t)(kStages - 1) * stride, (it + kStages - 1) % kStages, true);
-        while (chunk >= bi_next) {
-            bi++;
-            bi_start = B.start[bi];
-            bi_next = bi + 1 < B.n ? B.start[bi + 1] : nchunks;
+        uint64_t lchunk;
+        if (inter) {
+            bi = (uint32_t)(chunk % inter);
+            lchunk = chunk / inter;
+        } else {
+            while (chunk >= bi_next) {
+                bi++;
+                bi_start = B.start[bi];
+                bi_next = bi + 1 < B.n ? B.start[bi + 1] : nchunks;
+            }
+            lchunk = chunk - bi_start;
         }
-        const uint64_t lchunk = chunk - bi_start;
         const uint32_t d_in = B.d[bi];
         const float* __restrict__ x = B.x[bi];
         uint32_t* __restrict__ bitmap = B.bitmap[bi];

@@ -27,6 +27,11 @@ struct CompressBatch {
     uint64_t start[kMaxBatch + 1];
     uint32_t d[kMaxBatch];
     uint32_t n;
+    // 1: every input has the same d and the global chunk g is row-chunk g / n of
+    // input g % n — the n inputs' chunk i are compressed together, so their
+    // reductions into the same destination rows (the row maps depend only on the
+    // row) hit each sketch line while it is in L2
+    uint32_t interleave;
 };
 void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned long long* nnz_out,
                            cudaStream_t s);

@@ -1021,6 +1021,7 @@ int lhc_nvls_open(int rank, int world, const char* rendezvous, size_t bytes, lhc
     cudaFree(nullptr);  // the runtime's primary context is current
     CUdevice dev;
     if (CUresult r = cuDeviceGet_(&dev, ord)) return drv_err("cuDeviceGet", r);
+    auto cuMemRelease_ = DRV(cuMemRelease);
     CUmulticastObjectProp prop{};
     prop.numDevices = (unsigned)world;
     prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
@@ -1034,16 +1035,21 @@ int lhc_nvls_open(int rank, int world, const char* rendezvous, size_t bytes, lhc
     sockaddr_un addr;
     socklen_t alen;
     sock_addr(rendezvous, &addr, &alen);
+    // once the multicast object exists (created or imported), every failure releases it
+    auto release_mc = [&](int rc) {
+        if (mc && cuMemRelease_) cuMemRelease_(mc);
+        return rc;
+    };
     if (rank == 0) {
         if (CUresult r = cuMulticastCreate_(&mc, &prop)) return drv_err("cuMulticastCreate", r);
         int fd = -1;
         if (CUresult r = cuMemExport_(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0))
-            return drv_err("cuMemExportToShareableHandle", r);
+            return release_mc(drv_err("cuMemExportToShareableHandle", r));
         int ls = socket(AF_UNIX, SOCK_STREAM, 0);
         if (ls < 0 || bind(ls, (sockaddr*)&addr, alen) != 0 || listen(ls, world) != 0) {
             if (ls >= 0) close(ls);
             close(fd);
-            return set_error(LHC_ECOMM, "rendezvous socket '%s' unavailable", rendezvous);
+            return release_mc(set_error(LHC_ECOMM, "rendezvous socket '%s' unavailable", rendezvous));
         }
         for (int i = 1; i < world; i++) {
             int c = accept(ls, nullptr, nullptr);
@@ -1051,7 +1057,7 @@ int lhc_nvls_open(int rank, int world, const char* rendezvous, size_t bytes, lhc
                 if (c >= 0) close(c);
                 close(ls);
                 close(fd);
-                return set_error(LHC_ECOMM, "sending the multicast handle failed");
+                return release_mc(set_error(LHC_ECOMM, "sending the multicast handle failed"));
             }
             close(c);
         }
@@ -1076,7 +1082,7 @@ int lhc_nvls_open(int rank, int world, const char* rendezvous, size_t bytes, lhc
         close(fd);
         if (r) return drv_err("cuMemImportFromShareableHandle", r);
     }
-    if (CUresult r = cuMulticastAddDevice_(mc, dev)) return drv_err("cuMulticastAddDevice", r);
+    if (CUresult r = cuMulticastAddDevice_(mc, dev)) return release_mc(drv_err("cuMulticastAddDevice", r));
     lhc_nvls* h = new lhc_nvls();
     h->rank = rank;
     h->world = world;
@@ -1111,20 +1117,47 @@ int lhc_nvls_bind(lhc_nvls* h, void** local_ptr, size_t* size) {
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = h->dev;
     ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // as the multicast object
+    // a failure part-way unwinds what was done (mappings, reservations, binding,
+    // the allocation), leaving the handle open and unbound
+    auto cuMemUnmap_ = DRV(cuMemUnmap);
+    auto cuMemAddressFree_ = DRV(cuMemAddressFree);
+    auto cuMemRelease_ = DRV(cuMemRelease);
+    auto cuMulticastUnbind_ = DRV(cuMulticastUnbind);
+    bool created = false, bound_mc = false, uc_res = false, uc_map = false, mc_res = false, mc_map = false;
+    auto unwind = [&](int rc) {
+        if (mc_map && cuMemUnmap_) cuMemUnmap_(h->mc_va, h->size);
+        if (mc_res && cuMemAddressFree_) cuMemAddressFree_(h->mc_va, h->size);
+        if (uc_map && cuMemUnmap_) cuMemUnmap_(h->uc_va, h->size);
+        if (uc_res && cuMemAddressFree_) cuMemAddressFree_(h->uc_va, h->size);
+        CUdevice cd;
+        auto cuDeviceGet_ = DRV(cuDeviceGet);
+        if (bound_mc && cuMulticastUnbind_ && cuDeviceGet_ && !cuDeviceGet_(&cd, h->dev))
+            cuMulticastUnbind_(h->mc, cd, 0, h->size);
+        if (created && cuMemRelease_) cuMemRelease_(h->mem);
+        h->uc_va = h->mc_va = 0;
+        h->mem = 0;
+        return rc;
+    };
     if (CUresult r = cuMemCreate_(&h->mem, h->size, &ap, 0)) return drv_err("cuMemCreate", r);
-    if (CUresult r = cuMulticastBindMem_(h->mc, 0, h->mem, 0, h->size, 0)) return drv_err("cuMulticastBindMem", r);
+    created = true;
+    if (CUresult r = cuMulticastBindMem_(h->mc, 0, h->mem, 0, h->size, 0)) return unwind(drv_err("cuMulticastBindMem", r));
+    bound_mc = true;
     CUmemAccessDesc acc{};
     acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     acc.location.id = h->dev;
     acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    if (CUresult r = cuMemAddressReserve_(&h->uc_va, h->size, 0, 0, 0)) return drv_err("cuMemAddressReserve", r);
-    if (CUresult r = cuMemMap_(h->uc_va, h->size, 0, h->mem, 0)) return drv_err("cuMemMap", r);
-    if (CUresult r = cuMemSetAccess_(h->uc_va, h->size, &acc, 1)) return drv_err("cuMemSetAccess", r);
-    if (CUresult r = cuMemAddressReserve_(&h->mc_va, h->size, 0, 0, 0)) return drv_err("cuMemAddressReserve", r);
-    if (CUresult r = cuMemMap_(h->mc_va, h->size, 0, h->mc, 0)) return drv_err("cuMemMap(multicast)", r);
-    if (CUresult r = cuMemSetAccess_(h->mc_va, h->size, &acc, 1)) return drv_err("cuMemSetAccess(multicast)", r);
+    if (CUresult r = cuMemAddressReserve_(&h->uc_va, h->size, 0, 0, 0)) return unwind(drv_err("cuMemAddressReserve", r));
+    uc_res = true;
+    if (CUresult r = cuMemMap_(h->uc_va, h->size, 0, h->mem, 0)) return unwind(drv_err("cuMemMap", r));
+    uc_map = true;
+    if (CUresult r = cuMemSetAccess_(h->uc_va, h->size, &acc, 1)) return unwind(drv_err("cuMemSetAccess", r));
+    if (CUresult r = cuMemAddressReserve_(&h->mc_va, h->size, 0, 0, 0)) return unwind(drv_err("cuMemAddressReserve", r));
+    mc_res = true;
+    if (CUresult r = cuMemMap_(h->mc_va, h->size, 0, h->mc, 0)) return unwind(drv_err("cuMemMap(multicast)", r));
+    mc_map = true;
+    if (CUresult r = cuMemSetAccess_(h->mc_va, h->size, &acc, 1)) return unwind(drv_err("cuMemSetAccess(multicast)", r));
     if (cudaMemset((void*)h->uc_va, 0, h->size) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
-        return set_error(LHC_ECUDA, "clearing the NVLS buffer failed");
+        return unwind(set_error(LHC_ECUDA, "clearing the NVLS buffer failed"));
     h->bound = 1;
     if (local_ptr) *local_ptr = (void*)h->uc_va;
     if (size) *size = h->size - kNvlsSig;

@@ -49,6 +49,9 @@ namespace lhc {
 #define LHC_PEEL_THREADS 512
 #endif
 constexpr int kPeelThreads = LHC_PEEL_THREADS;
+#ifndef LHC_PEEL_MINB
+#define LHC_PEEL_MINB 1
+#endif
 
 __device__ __forceinline__ uint32_t cand_cell(const KParams& P, const uint2* __restrict__ tabS,
                                               uint32_t p, uint32_t j, uint32_t* neg) {
@@ -552,7 +555,7 @@ __device__ __forceinline__ void zero_dense(float* dense, uint32_t d, uint64_t gt
 // row, 2 = compact state prebuilt by destination row (falls back to mode 0 if the
 // build flagged a row with too many input rows).
 template <int KT>
-__global__ void __launch_bounds__(kPeelThreads)
+__global__ void __launch_bounds__(kPeelThreads, LHC_PEEL_MINB)
 k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
        const uint32_t* __restrict__ cand, float* dense, uint64_t cap, void* cells_v,
        uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,

@@ -184,6 +184,49 @@ def test_compress_coo_out_of_range_flagged(lhc, ora, index):
     assert not U(bm[p.words:]).any() and not F(ct[int(p.c):]).any()
 
 
+@pytest.mark.parametrize("law", ["dyadic", "gauss"])
+def test_negative_zero_and_exact_cancellation(lhc, ora, law):
+    """R22: -0.0 is a zero (not inserted; "true indicates non-zero"); R12:
+    coordinates where the workers' values cancel exactly stay candidates and recover
+    an exact 0 (footnote P:L188).  Everything against the oracle."""
+    d, nnz, W, L = 200_003, 3_000, 3, 1024
+    s = lhc.size_workload(d, nnz / d, W, L=L)
+    p = gpu_params(lhc, d, s.m, s.c, L=L, seed=0xC0C0)
+    xs = make_workers(d, nnz, W, 4242, law)
+    rng = rng_for(99)
+    # -0.0 at zeros of every worker (still zeros)
+    for x in xs:
+        zeros = np.flatnonzero(x == 0)
+        x[rng.choice(zeros, 500, replace=False)] = -0.0
+    # exact cancellation between workers 0 and 1 at 200 coordinates only they hold
+    only = np.flatnonzero((xs[0] == 0) & (xs[1] == 0) & (xs[2] == 0))
+    pos = rng.choice(only, 200, replace=False)
+    v = values(rng, 200, "dyadic")
+    xs[0][pos] = v
+    xs[1][pos] = -v
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    B, Y, ref = ora.pipeline(ora_params(ora, p), xs)
+    assert np.array_equal(U(run.sketch.bitmap), B)
+    st = compare_decode(ora, dec, ref, exact=(law == "dyadic"))
+    assert st["success"]
+    cand = set(ref.cand.tolist())
+    assert all(int(q) in cand for q in pos)       # cancelled coordinates stay candidates ...
+    dense = F(dec.dense)
+    assert np.all(dense[pos] == 0.0)              # ... and recover an exact 0
+    # -0.0 coordinates set no index bit: with the exact bitmap they are not candidates
+    from paper_2402_07529_b200.sizing import INDEX_BITMAP
+
+    pb = gpu_params(lhc, d, -(-d // L) * L, s.c, kb=INDEX_BITMAP, L=L, seed=0xC0C1)
+    runb = lhc.LosslessAllReduce(pb, cap_cand=d, local_workers=W)
+    decb = runb.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    nb = decb.read_stats()["n_cand"]
+    support = np.flatnonzero(np.any(np.stack(xs) != 0, axis=0))  # -0.0 != 0 is False
+    assert np.array_equal(U(decb.idx[:nb]), support.astype(np.uint32))
+
+
 def test_aggregate(lhc, ora):
     d, L, W = 500_000, 1024, 5
     s = lhc.size_workload(d, 0.01, W)
@@ -438,28 +481,36 @@ FULL = [
     ("ncf", {"index": "bitmap"}),
     ("lstm", {}),
     ("bert", {"density": 0.01}),
+    ("bert", {"density": 0.02}),
+    ("bert", {"density": 0.05}),
     ("bert", {"density": 0.10}),
+    ("bert", {"workers": 2}),
+    ("bert", {"workers": 4}),
     ("vgg", {}),
+    ("vgg", {"per_worker": True}),
 ]
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("name,over", FULL,
-                         ids=[f"{n}-{o.get('density', '')}{o.get('index', '')}" for n, o in FULL])
+                         ids=[f"{n}-" + "-".join(f"{k}{v}" for k, v in o.items()) for n, o in FULL])
 def test_full_size_configs(lhc, ora, name, over):
-    """The bench's launch configuration (per-worker sketches aggregated on one GPU,
-    one decode) at the configs' full sizes, compared in full with the oracle."""
+    """The bench's launch configuration (all of a rank's workers compressed into its
+    one sketch, one decode; or per-worker sketches aggregated on the GPU) at the
+    configs' full sizes — BERT over its 1/2/5/10 % density and 2/4/8-worker sweeps —
+    compared in full with the oracle."""
     from paper_2402_07529_b200.sizing import INDEX_BITMAP
 
     over = dict(over)
     kb = INDEX_BITMAP if over.pop("index", "bloom") == "bitmap" else 0
+    per_worker = over.pop("per_worker", False)
     wl = config(name, **over)
     s = lhc.size_workload(wl.d, wl.density, wl.workers, k_bloom=kb)
     p = gpu_params(lhc, wl.d, s.m, s.c, kb=kb, seed=0x1DC0DE)
     op = ora_params(ora, p)
     xs = [wl.dense(w) for w in range(wl.workers)]
     run = lhc.LosslessAllReduce(p, cap_cand=int(s.n_cand_expected * 1.5) + 1024,
-                                local_workers=wl.workers)
+                                local_workers=wl.workers, per_worker=per_worker)
     dec = run.step([torch.from_numpy(x).cuda() for x in xs])
     torch.cuda.synchronize()
     B, Y, ref = ora.pipeline(op, xs)

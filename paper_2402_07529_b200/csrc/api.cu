@@ -372,9 +372,18 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
         if (eb != cudaSuccess) return set_error(LHC_ECUDA, "blocked peel launch: %s", cudaGetErrorString(eb));
         mode = 3;
     }
-    if (mode == 1 || mode == 2)
+    if (mode == 1 || mode == 2) {
+        // the dense output is zeroed before the state is built, so that the 4d-byte
+        // write does not evict the freshly built state from L2 before the rounds
+        // (the peel then skips its in-kernel zeroing: mode | 8)
+        const char* ez = getenv("LHC_ZERO_FIRST");
+        if (!(ez && !strcmp(ez, "0"))) {
+            cudaMemsetAsync(dense, 0, (size_t)v.P.d * sizeof(float), s);
+            mode |= 8;
+        }
         launch_build_cells(v.P, counters, v.tabS, v.gmask, v.dst_off, v.pair_pos, v.dst_list,
-                           v.cells, v.ctrl, mode == 2, s);
+                           v.cells, v.ctrl, (mode & 7) == 2, s);
+    }
     cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, dense, cap_cand, v.cells, v.claim,
                                 v.frontier, v.ctrl, out_val, out_peeled, stats, mode, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));

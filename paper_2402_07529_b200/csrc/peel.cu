@@ -582,6 +582,8 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
     if (threadIdx.x == 0) { sh_n = 0; sh_peeled = 0; }
     if (timer) ctrl->t[0] = globaltimer();
+    const bool prezeroed = mode & 8;  // the launcher zeroed the dense output already
+    mode &= 7;
     if (mode == 2 && *(volatile uint32_t*)&ctrl->compact_fail) mode = 0;  // uniform
     if (mode == 3) {  // fallback after the blocked peel: only if a block could not be peeled
         if (!*(volatile uint32_t*)&ctrl->blk_fail) return;
@@ -590,7 +592,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     __syncthreads();
     // claim bits cleared (ordered before the rounds by the grid barriers below)
     for (uint64_t w = gtid; w < ((uint64_t)P.d + 31) / 32; w += gstride) __stcg(claim + w, 0u);
-    if (mode != 0) zero_dense(dense, P.d, gtid, gstride);
+    if (mode != 0 && !prezeroed) zero_dense(dense, P.d, gtid, gstride);
 
     if (mode == 0) {
         CellState* cells = static_cast<CellState*>(cells_v);

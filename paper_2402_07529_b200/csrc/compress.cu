@@ -54,7 +54,7 @@ void launch_hash_rows(const KParams& P, uint32_t dom, uint64_t n_rows, uint2* ou
 // gradient does not evict the sketch lines they accumulate into.
 // ---------------------------------------------------------------------------
 #ifndef LHC_COMPRESS_WARPS
-#define LHC_COMPRESS_WARPS 16
+#define LHC_COMPRESS_WARPS 8
 #endif
 #ifndef LHC_COMPRESS_STAGES
 #define LHC_COMPRESS_STAGES 2
@@ -128,7 +128,13 @@ k_compress_dense(KParams P, const __grid_constant__ CompressBatch B,
     const uint64_t nchunks = B.start[B.n];  // chunks of all inputs
     const uint64_t stride = (uint64_t)gridDim.x * kCompressWarps;
     const uint64_t first = blockIdx.x * (uint64_t)kCompressWarps + warp;
-    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+#ifndef LHC_COMPRESS_POL
+#define LHC_COMPRESS_POL 0
+#endif
+    uint64_t pol_keep, pol_stream, pol_norm;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_norm));
+    pol_keep = (LHC_COMPRESS_POL & 1) ? pol_norm : policy_evict_last();
+    pol_stream = (LHC_COMPRESS_POL & 2) ? pol_norm : policy_evict_first();
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t my_nnz = 0;
 

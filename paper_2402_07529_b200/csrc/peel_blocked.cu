@@ -61,7 +61,8 @@ __host__ __device__ inline size_t blk_smem_words(const KParams& P, uint32_t rpb)
            + (size_t)P.k * P.S_Y                           // input rows per destination row
            + 2 * (size_t)rpb * P.k + 1                     // row maps (uint2) of the block's rows
            + (size_t)rpb * P.nw                            // block-local index of each word's first candidate
-           + cb;                                           // values of the block's candidates
+           + cb                                            // values of the block's candidates
+           + 2 * ((cb + 31) / 32);                         // cells to examine: this round's, the next's
 }
 
 __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_constant__ BlkArgs A) {
@@ -80,6 +81,8 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
     uint2* maps = reinterpret_cast<uint2*>(sm + maps_off);                             // [rpb][k]
     uint32_t* wpre = reinterpret_cast<uint32_t*>(maps + (size_t)A.rpb * k);            // [rpb][nw]
     float* cval = reinterpret_cast<float*>(wpre + (size_t)A.rpb * nw);                 // [cb]
+    const uint32_t ncw = (cb + 31) / 32;                   // words of a cell bitmask
+    uint32_t* touch = reinterpret_cast<uint32_t*>(cval + cb);                          // [2][ncw]
     __shared__ uint32_t sh_warp[32];
     __shared__ uint32_t sh_nb;
     const uint32_t cells_per_thread = (cb + blockDim.x - 1) / blockDim.x;  // <= kBlkCellsPerThread
@@ -186,18 +189,37 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
         const bool staged = sh_nb <= cb;
         if (LHC_BLK_TIMING && threadIdx.x == 0) tb2 = globaltimer();
         // ---- synchronous rounds
-        for (;;) {
-            // A: pure cells at the start of the round (thread-strided, <= 32 per thread)
+        // Only a cell whose degree dropped to one in the previous round can be pure in
+        // this one (every pure cell's candidate is peeled in its round), so a round
+        // examines the cells marked in its bitmask (all cells in round 1) and marks
+        // for the next round the cells its removals bring from degree two to one.
+        // Thread t examines the cells [t*cpt, (t+1)*cpt).
+        for (uint32_t a = threadIdx.x; a < 2 * ncw; a += blockDim.x) touch[a] = a < ncw ? ~0u : 0u;
+        __syncthreads();
+        unsigned long long tb_round = LHC_BLK_TIMING ? globaltimer() : 0ull;
+        for (uint32_t cur = 0;; cur ^= 1u) {
+            uint32_t* tc = touch + cur * ncw;
+            uint32_t* tn = touch + (cur ^ 1u) * ncw;
+            // A: pure cells at the start of the round among the marked ones
+            const uint32_t c0 = threadIdx.x * cells_per_thread;
             uint32_t pure = 0u;
-            for (uint32_t s = 0; s < cells_per_thread; s++) {
-                const uint32_t e = threadIdx.x + s * blockDim.x;
-                if (e < cb && (key[e] >> 24) == 1u) pure |= 1u << s;
+            if (c0 < cb) {
+                const uint32_t w0 = c0 >> 5, sh = c0 & 31;
+                uint64_t bits = (uint64_t)tc[w0] | (w0 + 1 < ncw ? (uint64_t)tc[w0 + 1] << 32 : 0ull);
+                bits >>= sh;
+                uint32_t cand = (uint32_t)bits & (cells_per_thread >= 32 ? ~0u : ((1u << cells_per_thread) - 1u));
+                for (; cand; cand &= cand - 1) {
+                    const uint32_t s2 = __ffs(cand) - 1;
+                    if (c0 + s2 < cb && (key[c0 + s2] >> 24) == 1u) pure |= 1u << s2;
+                }
             }
             if (!__syncthreads_or(pure != 0u)) break;
+            // (this round's marks are read: clear them for the round after next)
+            for (uint32_t a = threadIdx.x; a < ncw; a += blockDim.x) tc[a] = 0u;
             // B: peel them
             uint32_t my_peeled = 0;
             for (uint32_t pm = pure; pm; pm &= pm - 1) {
-                const uint32_t e = threadIdx.x + (__ffs(pm) - 1) * blockDim.x;
+                const uint32_t e = c0 + (__ffs(pm) - 1);
                 const uint32_t kv = key[e];
                 if ((kv >> 24) != 1u) continue;  // its only candidate was peeled via another cell
                 const uint32_t id = kv & 0xffffffu;
@@ -208,7 +230,7 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
                 const uint2 mpe = maps[t * k + je];
                 const float val = map_sign(mpe) * R[e];
                 for (uint32_t j = 0; j < k; j++) {
-                    // every cell of p loses it (its pure cell too: degree 0, not rescanned)
+                    // every cell of p loses it (its pure cell too: degree 0, not marked)
                     if (j == je) {
                         atomicSub(&key[e], (1u << 24) + id);
                         continue;
@@ -216,7 +238,10 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
                     const uint2 mp = maps[t * k + j];
                     const uint32_t ej = (mp.x - rbase) * L + ((col + map_bias(mp)) & (L - 1));
                     atomicAdd(&R[ej], -map_sign(mp) * val);
-                    atomicSub(&key[ej], (1u << 24) + id);
+                    // the new key reads degree one exactly when it is one (the id sum of
+                    // two candidates may carry into the degree byte: test the new key)
+                    const uint32_t now = atomicSub(&key[ej], (1u << 24) + id) - ((1u << 24) + id);
+                    if ((now >> 24) == 1u) atomicOr(&tn[ej >> 5], 1u << (ej & 31));
                 }
                 const uint32_t ci = wpre[t * nw + w] + __popc(mask[t * nw + w] & (bit - 1u));
                 if (staged) {
@@ -233,6 +258,12 @@ __global__ void __launch_bounds__(kBlkThreads) k_peel_blocked(const __grid_const
             const uint32_t any = __syncthreads_or(my_peeled != 0u);
             if (my_peeled) atomicAdd(&sh_peeled, my_peeled);
             if (any && threadIdx.x == 0) sh_rounds++;
+            if (LHC_BLK_TIMING && threadIdx.x == 0 && sh_rounds < 128) {  // per round: time, peeled
+                const unsigned long long tr = globaltimer();
+                atomicAdd(&A.ctrl->tproc[sh_rounds], tr - tb_round);
+                atomicAdd(&A.ctrl->tflush[sh_rounds], (unsigned long long)sh_peeled);
+                tb_round = tr;
+            }
         }
         if (LHC_BLK_TIMING && threadIdx.x == 0) tb3 = globaltimer();
         // ---- finalize: median estimate of the block's unpeeled candidates

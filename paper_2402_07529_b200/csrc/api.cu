@@ -366,6 +366,20 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
         if (!strcmp(ev, "compact")) mode = v.P.nrows <= (1u << 22) ? 2 : 1, blocked = false;
         if (!strcmp(ev, "insert")) mode = 0, blocked = false;
     }
+    // large blocks, one per thread-block cluster with the state in distributed shared
+    // memory (peel_cluster.cu): correct but slower than the global peel on the same
+    // layout (VGG19, 82 blocks of 196,608 cells: 5.0 ms vs 2.2 ms — DSMEM atomics
+    // across 16 CTAs sustain ~56 G/s in total), so only on request (LHC_PEEL_CLUSTER=1)
+    const char* ecl = getenv("LHC_PEEL_CLUSTER");
+    uint32_t cl_size = v.P.blocks && ecl && !strcmp(ecl, "1") ? peel_cluster_size(v.P) : 0u;
+    if (getenv("LHC_CELL_BUILD")) cl_size = 0;
+    if (cl_size) {
+        cudaError_t ec = launch_peel_cluster(v.P, cl_size, counters, v.tabS, v.gmask, v.rowoff, dense,
+                                             cap_cand, out_val, out_peeled, v.ctrl, stats, s);
+        if (ec != cudaSuccess) return set_error(LHC_ECUDA, "cluster peel launch: %s", cudaGetErrorString(ec));
+        mode = 3;
+        blocked = false;
+    }
     if (blocked) {
         cudaError_t eb = launch_peel_blocked(v.P, counters, v.tabS, v.gmask, v.rowoff, dense, cap_cand,
                                              out_val, out_peeled, v.ctrl, stats, s);

@@ -55,6 +55,13 @@ cudaError_t launch_peel_blocked(const KParams& P, const float* counters, const u
                                 uint64_t cap, float* out_val, uint8_t* out_peeled, Ctrl* ctrl,
                                 lhc_stats* stats, cudaStream_t s);
 uint32_t query_max_ctas();
+// cluster-level (DSMEM) peel of a blocked sketch with large blocks (peel_cluster.cu):
+// the cluster size to use, or 0 when it does not apply
+uint32_t peel_cluster_size(const KParams& P);
+cudaError_t launch_peel_cluster(const KParams& P, uint32_t cs, const float* counters, const uint2* tabS,
+                                const uint32_t* gmask, const uint32_t* rowoff, float* dense,
+                                uint64_t cap, float* out_val, uint8_t* out_peeled, Ctrl* ctrl,
+                                lhc_stats* stats, cudaStream_t s);
 
 // peeling decoder (peel.cu)
 void launch_pair_lists(const KParams& P, const uint2* tabS, uint32_t* dst_off, uint32_t* pair_pos,

@@ -761,3 +761,31 @@ def test_pipeline_deterministic_decode(lhc, ora, d, nnz, W, L, structure, law):
     torch.cuda.synchronize()
     _, _, ref = ora.pipeline(ora_params(ora, p), xs)
     compare_decode(ora, dec, ref, law == "dyadic")
+
+
+@pytest.mark.parametrize("d,nnz,W,L,B,S,law", [
+    (3_000_017, 30_000, 3, 1024, 4, 16, "dyadic"),    # 16-CTA clusters, ragged tail
+    (3_000_017, 30_000, 3, 1024, 4, 16, "gauss"),
+    (2_000_000, 20_000, 2, 256, 6, 16, "dyadic"),     # 8-CTA clusters (L = 256)
+    (4_000_000, 60_000, 3, 1024, 2, 32, "dyadic"),    # near the threshold: many rounds
+    (1_000_000, 30_000, 2, 1024, 2, 16, "dyadic"),    # overloaded: stalls, median fallback
+])
+@pytest.mark.parametrize("impl", ["cluster", "global"])
+def test_cluster_blocked_peel(lhc, ora, d, nnz, W, L, B, S, law, impl, monkeypatch):
+    """P:L206 blocks large enough for a thread-block cluster: the block's decode state
+    lives in the cluster's distributed shared memory (peel_cluster.cu, on request), or
+    the global peel decodes the blocked layout.  Candidates, flags, rounds, success and
+    values (incl. the median fallback) equal the oracle's."""
+    if impl == "cluster":
+        monkeypatch.setenv("LHC_PEEL_CLUSTER", "1")
+    else:
+        monkeypatch.delenv("LHC_PEEL_CLUSTER", raising=False)
+    s = lhc.size_workload(d, nnz / d, W, L=L)
+    p = lhc.params(d, s.m, B * 3 * S * L, 3, 0, L, 0xC1C1 + d + B, B)
+    op = ora_params(ora, p)
+    xs = make_workers(d, nnz, W, 61 + B, law)
+    run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)
+    dec = run.step([torch.from_numpy(x).cuda() for x in xs])
+    torch.cuda.synchronize()
+    _, _, ref = ora.pipeline(op, xs)
+    compare_decode(ora, dec, ref, law == "dyadic")

@@ -21,9 +21,11 @@ def main():
     dev = torch.device("cuda", 0)
     for name in sys.argv[1:] or ["vgg"]:
         wl = config(name, law="gauss")
-        sz, nb = size_blocked(wl.d, wl.density, wl.workers, gamma=1.30, k_bloom=0, L=256,
-                              cells_per_block=12288)
-        p = lhc.params(wl.d, sz.m, sz.c, 3, 0, 256, 0x1DC0DE, nb)
+        L = int(os.environ.get("BLK_L", "256"))
+        cpb = int(os.environ.get("BLK_CELLS", "12288"))
+        sz, nb = size_blocked(wl.d, wl.density, wl.workers, gamma=1.30, k_bloom=0, L=L,
+                              cells_per_block=cpb)
+        p = lhc.params(wl.d, sz.m, sz.c, 3, 0, L, 0x1DC0DE, nb)
         xs = [torch.from_numpy(wl.dense(w)).to(dev) for w in range(wl.workers)]
         run = lhc.LosslessAllReduce(p, min(wl.d, int(sz.n_cand_expected * 1.05) + 4096),
                                     local_workers=len(xs), per_worker=False, device=dev)

@@ -201,7 +201,7 @@ def test_negative_zero_and_exact_cancellation(lhc, ora, law):
     # exact cancellation between workers 0 and 1 at 200 coordinates only they hold
     only = np.flatnonzero((xs[0] == 0) & (xs[1] == 0) & (xs[2] == 0))
     pos = rng.choice(only, 200, replace=False)
-    v = values(rng, 200, "dyadic")
+    v = values(rng, 200, law)  # same law as the rest (fp32 counters: |error| ~ |v| 2^-24)
     xs[0][pos] = v
     xs[1][pos] = -v
     run = lhc.LosslessAllReduce(p, cap_cand=d, local_workers=W)

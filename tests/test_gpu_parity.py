@@ -214,7 +214,10 @@ def test_negative_zero_and_exact_cancellation(lhc, ora, law):
     cand = set(ref.cand.tolist())
     assert all(int(q) in cand for q in pos)       # cancelled coordinates stay candidates ...
     dense = F(dec.dense)
-    assert np.all(dense[pos] == 0.0)              # ... and recover an exact 0
+    if law == "dyadic":                           # ... and recover an exact 0 (fp32 sums exact)
+        assert np.all(dense[pos] == 0.0)
+    else:                                         # ... or 0 within the tolerance (compare_decode)
+        assert np.all(np.abs(dense[pos]) <= ATOL)
     # -0.0 coordinates set no index bit: with the exact bitmap they are not candidates
     from paper_2402_07529_b200.sizing import INDEX_BITMAP
 

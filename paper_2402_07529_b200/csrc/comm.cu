@@ -348,8 +348,8 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
         for (uint64_t i = max(hi, 4 * e4) + rtid; i < A.d; i += rstride) A.dense[i] = 0.f;
     }
     sh_barrier<G>(grid, A, epoch + 1);
-#pragma unroll 1
     if (own_over) fill_shard_nan(A.dense, A.rank, A.shard_width, A.d, gtid, gstride);
+#pragma unroll 1
     for (int dd = 1; dd < G; dd++) {
         const int q = (A.rank + dd) % G;
         const uint32_t cnt = *(volatile uint32_t*)(A.sig[A.rank] + kGatherCountSlot + par * kMaxRanks + q);
@@ -474,7 +474,7 @@ extern "C" {
 
 int lhc_shard_layout(const lhc_params* ps, int world, uint64_t cap_items, size_t* slot_bytes,
                      size_t* counters_off, size_t* total_bytes) {
-    size_t slot, y, st, ga, sg, t;
+    size_t slot = 0, y = 0, st = 0, ga = 0, sg = 0, t = 0;
     if (int rc = shard_layout(ps, world, cap_items, &slot, &y, &st, &ga, &sg, &t)) return rc;
     if (slot_bytes) *slot_bytes = slot;
     if (counters_off) *counters_off = y;
@@ -611,7 +611,7 @@ int sketch_allreduce(lhc_comm* c, void* stream) {
 int lhc_shard_comm_create(int rank, int world, const void* handles, const uint64_t* offsets,
                           void* local_buf, size_t buf_bytes, const lhc_params* ps, uint64_t cap_items,
                           lhc_comm** out) {
-    size_t slot, y, st, ga, sg, t;
+    size_t slot = 0, y = 0, st = 0, ga = 0, sg = 0, t = 0;
     if (int rc = shard_layout(ps, world, cap_items, &slot, &y, &st, &ga, &sg, &t)) return rc;
     if (!out || !local_buf) return set_error(LHC_EINVAL, "NULL argument");
     if (rank < 0 || rank >= world) return set_error(LHC_EINVAL, "0 <= rank < world required");
@@ -1195,7 +1195,7 @@ int sketch_allreduce_nvls(lhc_nvls* h, const lhc_params* p, void* stream) {
 
 int sketch_reduce_scatter_nvls(lhc_nvls* h, const lhc_params* ps, uint64_t cap_items, void* stream) {
     if (!h || !h->bound) return set_error(LHC_EINVAL, "NVLS handle not bound");
-    size_t slot, y, st, ga, sg, t;
+    size_t slot = 0, y = 0, st = 0, ga = 0, sg = 0, t = 0;
     if (int rc = shard_layout(ps, h->world, cap_items, &slot, &y, &st, &ga, &sg, &t)) return rc;
     if (t > h->size - kNvlsSig) return set_error(LHC_ECAPACITY, "NVLS buffer too small for the shard layout");
     reset_launches();
@@ -1210,7 +1210,7 @@ int sketch_allgather_decoded_nvls(lhc_nvls* h, const lhc_params* ps, uint64_t ca
                                   const unsigned long long* n_items, uint64_t shard_width, uint32_t d,
                                   float* dense, void* stream) {
     if (!h || !h->bound) return set_error(LHC_EINVAL, "NVLS handle not bound");
-    size_t slot, y, st, ga, sg, t;
+    size_t slot = 0, y = 0, st = 0, ga = 0, sg = 0, t = 0;
     if (int rc = shard_layout(ps, h->world, cap_items, &slot, &y, &st, &ga, &sg, &t)) return rc;
     if (t > h->size - kNvlsSig) return set_error(LHC_ECAPACITY, "NVLS buffer too small for the shard layout");
     if (!idx || !val || !n_items || !dense) return set_error(LHC_EINVAL, "NULL argument");

@@ -278,8 +278,12 @@ int sketch_decompress(const lhc_params* p, const uint32_t* bitmap, const float* 
  * them in this order with the same ws and cap_cand):
  *   sketch_query  step 1 — candidates to out_idx, n_cand / overflow to stats
  *   sketch_peel   steps 2-3 — out_val, out_peeled, n_peeled / rounds / success,
- *                 and out_dense (nullable; the workspace holds a dense scratch
- *                 used when it is NULL): zeroed, then the values at candidates */
+ *                 and out_dense (nullable): every coordinate < d is written,
+ *                 the value at candidates and exactly 0 elsewhere; when NULL
+ *                 only the list outputs are produced.  The workspace includes
+ *                 a log of 8 bytes per candidate slot (peeled values bucketed
+ *                 by 1024-coordinate chunk) and a dense scratch for blocked
+ *                 sketches. */
 int sketch_query(const lhc_params* p, const uint32_t* bitmap, void* ws, size_t ws_bytes,
                  uint64_t cap_cand, uint32_t* out_idx, lhc_stats* stats, void* stream);
 int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_bytes,

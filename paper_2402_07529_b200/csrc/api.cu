@@ -1,6 +1,7 @@
 // api.cu — the C ABI of include/lhc.h: host-side validation, workspace layout and
 // launch sequencing.  All compute happens in the kernels of compress.cu,
 // aggregate.cu, query.cu, peel.cu and comm.cu; nothing here touches data.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -120,6 +121,10 @@ WsLayout ws_layout(const KParams& P, uint64_t cap) {
     W.pair_pos = o;  o = align_up(o + (size_t)P.nrows * P.k * sizeof(uint32_t), 256);
     W.dst_list = o;  o = align_up(o + (size_t)P.nrows * P.k * sizeof(uint32_t), 256);
     W.rowoff = o;    o = align_up(o + ((size_t)P.nrows + 1) * sizeof(uint32_t), 256);
+    // peeled (coordinate, value) pairs, bucketed by 1024-coordinate chunk at the
+    // chunk's candidate slots (one end pointer per chunk)
+    W.vlog = o;      o = align_up(o + std::max<uint64_t>(std::min<uint64_t>(cap, P.d), 1) * sizeof(uint2), 256);
+    W.vfill = o;     o = align_up(o + ((size_t)W.nchunks + 1) * sizeof(uint32_t), 256);
     // row peel (peel_rows.cu): claim masks per probe, per-row flags and worklists,
     // sorted destination-row lists (the fixed-point deductions use `cells`, the
     // remaining masks `claim`)
@@ -288,6 +293,8 @@ struct WsView {
     float* dense;
     uint32_t *dst_off, *pair_pos, *dst_list;
     uint32_t* rowoff;
+    uint2* vlog;
+    uint32_t* vfill;
     uint32_t *claim_k, *dmark, *dst_sorted, *ymark, *xl, *yl;
 };
 
@@ -302,6 +309,8 @@ int ws_view(const lhc_params* p, void* ws, size_t ws_bytes, uint64_t* cap_cand, 
         return set_error(LHC_ECAPACITY, "workspace too small: %zu < %zu bytes", ws_bytes, v->W.total);
     char* b = static_cast<char*>(ws);
     v->rowoff = reinterpret_cast<uint32_t*>(b + v->W.rowoff);
+    v->vlog = reinterpret_cast<uint2*>(b + v->W.vlog);
+    v->vfill = reinterpret_cast<uint32_t*>(b + v->W.vfill);
     v->ctrl = reinterpret_cast<Ctrl*>(b + v->W.ctrl);
     v->tabS = reinterpret_cast<uint2*>(b + v->W.tabS);
     v->gmask = reinterpret_cast<uint32_t*>(b + v->W.gmask);
@@ -386,20 +395,14 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
         if (eb != cudaSuccess) return set_error(LHC_ECUDA, "blocked peel launch: %s", cudaGetErrorString(eb));
         mode = 3;
     }
-    if (mode == 1 || mode == 2) {
-        // the dense output is zeroed before the state is built, so that the 4d-byte
-        // write does not evict the freshly built state from L2 before the rounds
-        // (the peel then skips its in-kernel zeroing: mode | 8)
-        const char* ez = getenv("LHC_ZERO_FIRST");
-        if (!(ez && !strcmp(ez, "0"))) {
-            cudaMemsetAsync(dense, 0, (size_t)v.P.d * sizeof(float), s);
-            mode |= 8;
-        }
+    if (mode == 1 || mode == 2)
         launch_build_cells(v.P, counters, v.tabS, v.gmask, v.dst_off, v.pair_pos, v.dst_list,
-                           v.cells, v.ctrl, (mode & 7) == 2, s);
-    }
-    cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, dense, cap_cand, v.cells, v.claim,
-                                v.frontier, v.ctrl, out_val, out_peeled, stats, mode, s);
+                           v.cells, v.ctrl, mode == 2, s);
+    // the global peel writes every coordinate of the dense output itself (chunk by
+    // chunk, after the rounds); with no dense output it writes only the list values
+    cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, out_dense, cap_cand, v.cells, v.claim,
+                                v.frontier, v.ctrl, out_val, out_peeled, stats, v.rowoff, v.vlog,
+                                v.vfill, mode, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_peel");
 }

@@ -81,7 +81,8 @@ void launch_build_cells(const KParams& P, const float* counters, const uint2* ta
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* cand, float* dense, uint64_t cap, void* cells,
                         uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* out_val,
-                        uint8_t* out_peeled, lhc_stats* stats, int mode, cudaStream_t s);
+                        uint8_t* out_peeled, lhc_stats* stats, const uint32_t* rowoff,
+                        uint2* vlog, uint32_t* vfill, int mode, cudaStream_t s);
 int l2_bytes();
 
 WsLayout ws_layout(const KParams& P, uint64_t cap);

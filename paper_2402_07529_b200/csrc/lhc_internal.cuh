@@ -132,7 +132,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Sub-allocation of the decompress workspace.
 struct WsLayout {
     size_t tabS, gmask, cta_total, cells, claim, frontier, dense, dst_off, pair_pos, dst_list, ctrl,
-        rowoff, claim_k, dmark, dst_sorted, ymark, xl, yl, total;
+        rowoff, vlog, vfill, claim_k, dmark, dst_sorted, ymark, xl, yl, total;
     uint32_t nchunks;
 };
 

@@ -25,10 +25,15 @@
 //            set of candidates peeled per round, and the number of rounds, are
 //            exactly those of synchronous peeling.
 //   finalize unpeeled candidates take the median over j of sign_j * R;
-//            the candidate list's values are gathered from the dense output.
-// The dense output and the claim bits are zeroed inside the kernel before the
-// rounds (in build mode 0 while the key reductions drain), so every
-// non-candidate coordinate is exactly 0 without a memset or a densify pass.
+//            a warp per 1024-coordinate chunk assembles the chunk in shared memory
+//            (zeros, the chunk's peeled values, its medians), writes the list values
+//            of the chunk's candidate slots and the chunk of the dense output with
+//            full-line stores.
+// A peeled value is not stored at its coordinate during the rounds (a random 4-byte
+// store into the 4d-byte output costs a partial-sector read-modify-write in HBM):
+// it is appended as (coordinate, value) to its chunk's segment of a log whose
+// segments start at the chunk's first candidate slot (the query's row offsets), so
+// the appends of a chunk fill whole lines and the finalize reads them back in order.
 // Queue appends are aggregated per CTA in shared memory (one global atomic per
 // CTA per pass); every cell enters the queue at most once (c entries).
 #include <cooperative_groups.h>
@@ -363,6 +368,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                           const uint32_t* __restrict__ cand, float* dense, void* cells_v,
                           uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
                           uint8_t* __restrict__ out_peeled, lhc_stats* stats, uint64_t n_c,
+                          const uint32_t* __restrict__ rowoff, uint2* vlog, uint32_t* vfill,
                           uint2* sh_q, uint32_t* sh_n, uint32_t* sh_base, uint32_t* sh_peeled) {
     using C = Cells<COMPACT>;
     using Cell = typename C::T;
@@ -374,7 +380,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
-    const uint64_t pl = pol_last(), pf = pol_first();
+    const uint64_t pl = pol_last();
 
     // F0 ("round 0"): cells of degree one with their candidate, through rc[0]
     {
@@ -463,7 +469,14 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                         if (ev[j] == e) ge = map_sign(mp[j]);
                     }
                     const float val = ge * Re;
-                    st_hint(dense + p, val, pf);  // the value lands at its coordinate
+                    // the value's place in its chunk's log segment: one L2-resident
+                    // counter per chunk, one atomic per chunk and warp (runs of
+                    // candidates peel together); the store waits behind the key atomics
+                    const uint32_t q = p >> 10, lane = threadIdx.x & 31;
+                    const uint32_t peers = __match_any_sync(__activemask(), q);
+                    const uint32_t leader = __ffs(peers) - 1;
+                    uint32_t lbase = 0;
+                    if (lane == leader) lbase = atomicAdd(vfill + q, (uint32_t)__popc(peers));
                     atomicAdd(sh_peeled, 1u);
                     // all reductions first (independent), then the queue appends
                     const K dec = (K)0 - C::one(COMPACT ? i : p);
@@ -476,6 +489,8 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                         red_add_hint(&cells[ev[j]].R, -map_sign(mp[j]) * val, pl);
                         rest[j] = atom_add_hint(&cells[ev[j]].key, dec, pl) + dec;
                     }
+                    lbase = __shfl_sync(peers, lbase, leader) + __popc(peers & ((1u << lane) - 1u));
+                    vlog[lbase] = make_uint2(p, __float_as_uint(val));
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
@@ -505,50 +520,116 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
     }
     if (timer) ctrl->t[kCtrlTimes - 1] = globaltimer();
 
-    // finalize: median estimate of unpeeled candidates; four slots per
-    // thread with their loads in flight together
-    for (uint64_t s0 = gtid; s0 < n_c; s0 += 4 * gstride) {
-        uint32_t pp[4], cw[4];
-        float dv[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const uint64_t s = s0 + u * gstride;
-            pp[u] = s < n_c ? __ldg(cand + s) : 0u;
+    // finalize, a warp per 1024-coordinate chunk q with a 4 KB tile in shared memory
+    // (the queue buffer is free now): the chunk's candidates hold slots [s0, s1) of the
+    // list, its peeled values are log entries [s0, vfill[q]).  Unpeeled candidates
+    // take the median over j of sign_j * R.
+    {
+        const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+        float* tile = reinterpret_cast<float*>(sh_q) + wib * (kTile + 32);
+        uint32_t* pm = reinterpret_cast<uint32_t*>(tile + kTile);  // peeled bits of the chunk
+        const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
+        const uint32_t rsh = 10 - P.log2L;  // input rows per chunk = 2^rsh
+        const uint64_t gw = gtid >> 5, nwarps = gstride >> 5;
+        // the next chunk's bounds are loaded while this one is assembled; the first
+        // 128 log entries and 128 candidate slots of a chunk are loaded together
+        uint32_t n_s0 = 0, n_s1 = 0, n_f1 = 0;
+        if (gw < nchunks) {
+            n_s0 = __ldcg(rowoff + (gw << rsh));
+            n_s1 = gw + 1 < nchunks ? __ldcg(rowoff + ((gw + 1) << rsh)) : (uint32_t)n_c;
+            n_f1 = __ldcg(vfill + gw);
         }
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            cw[u] = s0 + u * gstride < n_c ? __ldcg(claim + (pp[u] >> 5)) : 0u;
-            dv[u] = s0 + u * gstride < n_c ? __ldcg(dense + pp[u]) : 0.f;
-        }
-#pragma unroll 1
-        for (int u = 0; u < 4; u++) {
-        const uint64_t s = s0 + u * gstride;
-        if (s >= n_c) break;
-        const uint32_t p = pp[u];
-        const bool pe = (cw[u] >> (p & 31)) & 1u;
-        out_peeled[s] = pe ? 1 : 0;
-        float val;
-        if (pe) {
-            val = dv[u];
-        } else {
-            float v[NJ];
-            for (uint32_t j = 0; j < k; j++) {
-                uint32_t neg;
-                const uint32_t e = cand_cell(P, tabS, p, j, &neg);
-                v[j] = (neg ? -1.f : 1.f) * __ldcg(&cells[e].R);
+        for (uint64_t q = gw; q < nchunks; q += nwarps) {
+            const uint32_t s0 = n_s0, s1 = n_s1, f1 = n_f1;
+            const uint64_t qn = q + nwarps;
+            if (qn < nchunks) {
+                n_s0 = __ldcg(rowoff + (qn << rsh));
+                n_s1 = qn + 1 < nchunks ? __ldcg(rowoff + ((qn + 1) << rsh)) : (uint32_t)n_c;
+                n_f1 = __ldcg(vfill + qn);
             }
-            for (uint32_t a = 1; a < k; a++) {  // insertion sort of <= 8 values
-                float x = v[a];
-                int b = (int)a - 1;
-                while (b >= 0 && v[b] > x) { v[b + 1] = v[b]; b--; }
-                v[b + 1] = x;
+            uint2 ent[4];
+            uint32_t pc[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t a = s0 + lane + 32 * u;
+                ent[u] = a < f1 ? __ldcs(vlog + a) : make_uint2(0u, 0u);
+                pc[u] = a < s1 ? __ldg(cand + a) : 0u;
             }
-            val = (k & 1) ? v[k / 2] : 0.5f * (v[k / 2 - 1] + v[k / 2]);
-            dense[p] = val;
-        }
-        out_val[s] = val;
+            float4* t4 = reinterpret_cast<float4*>(tile);
+#pragma unroll
+            for (int u = 0; u < 8; u++) t4[lane + 32 * u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            pm[lane] = 0u;
+            __syncwarp();
+            for (uint32_t a0 = s0;;) {
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (a0 + lane + 32 * u < f1) {
+                        const uint32_t off = ent[u].x & (kTile - 1);
+                        tile[off] = __uint_as_float(ent[u].y);
+                        atomicOr(pm + (off >> 5), 1u << (off & 31));
+                    }
+                a0 += 128;
+                if (a0 >= f1) break;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t a = a0 + lane + 32 * u;
+                    ent[u] = a < f1 ? __ldcs(vlog + a) : make_uint2(0u, 0u);
+                }
+            }
+            __syncwarp();
+            for (uint32_t a0 = s0;;) {
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t sl = a0 + lane + 32 * u;
+                    if (sl >= s1) continue;
+                    const uint32_t p = pc[u];
+                    const uint32_t off = p & (kTile - 1);
+                    const bool pe = (pm[off >> 5] >> (off & 31)) & 1u;
+                    float val;
+                    if (pe) {
+                        val = tile[off];
+                    } else {
+                        float v[NJ];
+                        for (uint32_t j = 0; j < k; j++) {
+                            uint32_t neg;
+                            const uint32_t e = cand_cell(P, tabS, p, j, &neg);
+                            v[j] = (neg ? -1.f : 1.f) * __ldcg(&cells[e].R);
+                        }
+                        for (uint32_t a = 1; a < k; a++) {  // insertion sort of <= 8 values
+                            float x = v[a];
+                            int b = (int)a - 1;
+                            while (b >= 0 && v[b] > x) { v[b + 1] = v[b]; b--; }
+                            v[b + 1] = x;
+                        }
+                        val = (k & 1) ? v[k / 2] : 0.5f * (v[k / 2 - 1] + v[k / 2]);
+                        tile[off] = val;
+                    }
+                    out_peeled[sl] = pe ? 1 : 0;
+                    out_val[sl] = val;
+                }
+                a0 += 128;
+                if (a0 >= s1) break;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t a = a0 + lane + 32 * u;
+                    pc[u] = a < s1 ? __ldg(cand + a) : 0u;
+                }
+            }
+            __syncwarp();
+            if (dense) {
+                const uint64_t c0 = q * kTile;
+                if (c0 + kTile <= P.d) {
+                    float4* o4 = reinterpret_cast<float4*>(dense + c0);
+#pragma unroll
+                    for (int u = 0; u < 8; u++) __stcs(o4 + lane + 32 * u, t4[lane + 32 * u]);
+                } else {
+                    for (uint32_t a = lane; c0 + a < P.d; a += 32) dense[c0 + a] = tile[a];
+                }
+            }
+            __syncwarp();  // the tile is read before the next chunk clears it
         }
     }
+    if (LHC_PEEL_TIMING && threadIdx.x == 0) atomicMax(&ctrl->t[1], globaltimer());
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         stats->n_peeled = n_peeled;
         stats->rounds = rounds;
@@ -556,14 +637,6 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
         stats->entries = f_end;  // every entry appended was processed by a round
         ctrl->rounds_dbg = rounds;
     }
-}
-
-// dense[0, d) = 0 with streaming 16-byte stores (dense is 16-byte aligned)
-__device__ __forceinline__ void zero_dense(float* dense, uint32_t d, uint64_t gtid, uint64_t gstride) {
-    float4* d4 = reinterpret_cast<float4*>(dense);
-    const uint64_t n4 = d / 4;
-    for (uint64_t u = gtid; u < n4; u += gstride) __stcs(d4 + u, make_float4(0.f, 0.f, 0.f, 0.f));
-    for (uint64_t i = 4 * n4 + gtid; i < d; i += gstride) dense[i] = 0.f;
 }
 
 // KT: compile-time k (3) or 0 for a run-time k <= kMaxK.  mode: 0 = build the wide
@@ -575,7 +648,8 @@ __global__ void __launch_bounds__(kPeelThreads, LHC_PEEL_MINB)
 k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
        const uint32_t* __restrict__ cand, float* dense, uint64_t cap, void* cells_v,
        uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
-       uint8_t* __restrict__ out_peeled, lhc_stats* stats, int mode) {
+       uint8_t* __restrict__ out_peeled, lhc_stats* stats, const uint32_t* __restrict__ rowoff,
+       uint2* vlog, uint32_t* vfill, int mode) {
     cg::grid_group grid = cg::this_grid();
     constexpr uint32_t NJ = KT ? KT : kMaxK;
     // queue buffer: kPeelThreads * peel_q_per_thread(k) entries of dynamic smem
@@ -598,17 +672,19 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
     if (threadIdx.x == 0) { sh_n = 0; sh_peeled = 0; }
     if (timer) ctrl->t[0] = globaltimer();
-    const bool prezeroed = mode & 8;  // the launcher zeroed the dense output already
-    mode &= 7;
     if (mode == 2 && *(volatile uint32_t*)&ctrl->compact_fail) mode = 0;  // uniform
     if (mode == 3) {  // fallback after the blocked peel: only if a block could not be peeled
         if (!*(volatile uint32_t*)&ctrl->blk_fail) return;
         mode = 0;
     }
     __syncthreads();
-    // claim bits cleared (ordered before the rounds by the grid barriers below)
+    // claim bits cleared and the log segments' ends set to their chunks' first slots
+    // (ordered before the rounds by the grid barriers below)
     for (uint64_t w = gtid; w < ((uint64_t)P.d + 31) / 32; w += gstride) __stcg(claim + w, 0u);
-    if (mode != 0 && !prezeroed) zero_dense(dense, P.d, gtid, gstride);
+    {
+        const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
+        for (uint64_t q = gtid; q < nchunks; q += gstride) vfill[q] = __ldcg(rowoff + (q << (10 - P.log2L)));
+    }
 
     if (mode == 0) {
         CellState* cells = static_cast<CellState*>(cells_v);
@@ -646,23 +722,26 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
                 atomicAdd(&cells[e2].key, (1ull << 32) + p);
             }
         }
-        // the dense output is zeroed while the reductions drain (fire-and-forget
-        // stores behind L2-bound atomics)
-        zero_dense(dense, P.d, gtid, gstride);
         grid.sync();
     }
     if (timer) ctrl->t[2] = globaltimer();
     if (mode == 2)
         peel_body<KT, true>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
-                            out_peeled, stats, n_c, sh_q, &sh_n, &sh_base, &sh_peeled);
+                            out_peeled, stats, n_c, rowoff, vlog, vfill, sh_q, &sh_n, &sh_base,
+                            &sh_peeled);
     else
         peel_body<KT, false>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
-                             out_peeled, stats, n_c, sh_q, &sh_n, &sh_base, &sh_peeled);
+                             out_peeled, stats, n_c, rowoff, vlog, vfill, sh_q, &sh_n, &sh_base,
+                             &sh_peeled);
 }
 
 constexpr uint64_t kSmallPeelCells = 1ull << 20;
 
-static size_t peel_smem(uint32_t k) { return (size_t)kPeelThreads * peel_q_per_thread(k) * sizeof(uint2); }
+// the queue buffer, reused by the finalize as one 4 KB tile (+ 128 B of bits) per warp
+static size_t peel_smem(uint32_t k) {
+    return std::max((size_t)kPeelThreads * peel_q_per_thread(k) * sizeof(uint2),
+                    (size_t)(kPeelThreads / 32) * (kTile + 32) * sizeof(float));
+}
 
 template <int KT>
 static int peel_grid(int dev, uint32_t k, bool small) {
@@ -683,7 +762,8 @@ static int peel_grid(int dev, uint32_t k, bool small) {
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* cand, float* dense, uint64_t cap, void* cells,
                         uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* out_val,
-                        uint8_t* out_peeled, lhc_stats* stats, int mode, cudaStream_t s) {
+                        uint8_t* out_peeled, lhc_stats* stats, const uint32_t* rowoff,
+                        uint2* vlog, uint32_t* vfill, int mode, cudaStream_t s) {
 #ifdef LHC_DEBUG_SYNC
     if (getenv("LHC_DEBUG_SKIP_PEEL")) return cudaSuccess;
 #endif
@@ -694,7 +774,7 @@ cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* ta
     void* args[] = {(void*)&Pc,    (void*)&counters, (void*)&tabS,    (void*)&cand,
                     (void*)&dense, (void*)&cap,      (void*)&cells,   (void*)&claim,
                     (void*)&frontier, (void*)&ctrl,  (void*)&out_val, (void*)&out_peeled,
-                    (void*)&stats, (void*)&mode};
+                    (void*)&stats, (void*)&rowoff, (void*)&vlog, (void*)&vfill, (void*)&mode};
     cudaError_t err;
     if (P.k == 3)
         err = cudaLaunchCooperativeKernel((const void*)k_peel<3>, dim3(peel_grid<3>(dev, 3, small)),

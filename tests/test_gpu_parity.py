@@ -255,12 +255,12 @@ def test_aggregate(lhc, ora):
 
 # ---------------------------------------------------------------- decompress --
 
-def run_decode(lhc, p, B, Y, cap=None, dense=True):
+def run_decode(lhc, p, B, Y, cap=None, dense=True, det=False):
     """Decode oracle-independent sketch bytes B (u32) / Y (fp32) on the GPU."""
     sk = lhc.Sketch(p)
     sk.bitmap.copy_(torch.from_numpy(B.view(np.int32)))
     sk.counters.copy_(torch.from_numpy(Y.astype(np.float32)))
-    dec = lhc.Decoder(p, cap if cap is not None else p.d, dense=dense)
+    dec = lhc.Decoder(p, cap if cap is not None else p.d, dense=dense, deterministic=det)
     dec(sk)
     torch.cuda.synchronize()
     return dec
@@ -343,7 +343,8 @@ def test_decode_threshold_sweep(lhc, ora, gamma):
     compare_decode(ora, dec, ref, exact=True)
 
 
-def test_overflow_and_caps(lhc, ora):
+@pytest.mark.parametrize("det", [False, True])
+def test_overflow_and_caps(lhc, ora, det):
     d, L = 300_000, 1024
     p = gpu_params(lhc, d, 3 * L * 8, 3 * L * 16, L=L, seed=3)
     op = ora_params(ora, p)
@@ -353,7 +354,7 @@ def test_overflow_and_caps(lhc, ora):
     n_c = len(ora.query(op, B))
     for cap in (10, n_c - 1, n_c, n_c + 5):
         ref = ora.decompress(op, B, Y, cap=cap)
-        dec = run_decode(lhc, p, B, Y, cap=cap)
+        dec = run_decode(lhc, p, B, Y, cap=cap, det=det)
         compare_decode(ora, dec, ref, exact=True)
 
 
@@ -389,13 +390,14 @@ def test_query_mask_patterns(lhc, ora, L):
         assert np.array_equal(U(dec.idx[:cap]), cand[:cap])
 
 
-def test_empty_and_degenerate(lhc, ora):
+@pytest.mark.parametrize("det", [False, True])
+def test_empty_and_degenerate(lhc, ora, det):
     L = 1024
     p = gpu_params(lhc, 5000, 3 * L, 3 * L, L=L, seed=1)
     op = ora_params(ora, p)
     B = np.zeros(p.words, np.uint32)
     Y = np.zeros(p.c, np.float64)
-    dec = run_decode(lhc, p, B, Y)
+    dec = run_decode(lhc, p, B, Y, det=det)
     st = dec.read_stats()
     assert st["n_cand"] == 0 and st["success"] and st["rounds"] == 0
     assert not F(dec.dense).any()
@@ -403,7 +405,7 @@ def test_empty_and_degenerate(lhc, ora):
     p1 = gpu_params(lhc, 1, 3 * 32, 3 * 32, L=32, seed=2)
     x = np.array([0.25], np.float32)
     B, Y, ref = ora.pipeline(ora_params(ora, p1), [x])
-    run = lhc.LosslessAllReduce(p1, cap_cand=1)
+    run = lhc.LosslessAllReduce(p1, cap_cand=1, deterministic=det)
     dec = run.step([torch.from_numpy(x).cuda()])
     torch.cuda.synchronize()
     compare_decode(ora, dec, ref, exact=True)

@@ -33,7 +33,8 @@ def main():
         t = np.frombuffer(raw[off_t:off_t + 128 * 8], dtype=np.uint64).astype(np.int64)
         fs = np.frombuffer(raw[off_t + 1024:off_t + 1024 + 512], dtype=np.uint32)
         print(f"== {name}: init {(t[2]-t[0])/1e3:.1f} us, F0 {(t[3]-t[2])/1e3:.1f} us, "
-              f"rounds to end {(t[127]-t[3])/1e3:.1f} us, stats {run.decoder.read_stats()}")
+              f"rounds to end {(t[127]-t[3])/1e3:.1f} us, "
+              f"finalize {((t[1]-t[127])/1e3 if t[1] else float('nan')):.1f} us, stats {run.decoder.read_stats()}")
         rows = []
         for r in range(1, 100):
             if not t[r + 3]:

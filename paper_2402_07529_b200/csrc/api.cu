@@ -397,7 +397,7 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
     }
     if (mode == 1 || mode == 2)
         launch_build_cells(v.P, counters, v.tabS, v.gmask, v.dst_off, v.pair_pos, v.dst_list,
-                           v.cells, v.ctrl, mode == 2, s);
+                           v.cells, v.ctrl, mode == 2, v.frontier, s);
     // the global peel writes every coordinate of the dense output itself (chunk by
     // chunk, after the rounds); with no dense output it writes only the list values
     cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, out_dense, cap_cand, v.cells, v.claim,

@@ -55,7 +55,7 @@ namespace lhc {
 #endif
 constexpr int kPeelThreads = LHC_PEEL_THREADS;
 #ifndef LHC_PEEL_MINB
-#define LHC_PEEL_MINB 1
+#define LHC_PEEL_MINB 2  // 64 registers: two 512-thread CTAs per SM
 #endif
 
 __device__ __forceinline__ uint32_t cand_cell(const KParams& P, const uint2* __restrict__ tabS,
@@ -231,7 +231,8 @@ template <bool COMPACT>
 __global__ void __launch_bounds__(256, LHC_BUILD_MINB)
 k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
               const uint32_t* __restrict__ gmask, const uint32_t* __restrict__ dst_off,
-              const uint32_t* __restrict__ dst_list, void* __restrict__ cells_v, Ctrl* ctrl) {
+              const uint32_t* __restrict__ dst_list, void* __restrict__ cells_v, Ctrl* ctrl,
+              uint2* __restrict__ frontier) {
     using Acc = typename std::conditional<COMPACT, uint32_t, unsigned long long>::type;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nw = P.nw;
@@ -286,6 +287,26 @@ k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __rest
                 }
             }
         }
+        // F0 fused: the row's cells of degree one are appended to the frontier queue
+        // (one reservation per row) as (cell, id) — id as in the peel's F0
+        uint32_t m1 = 0;
+#pragma unroll
+        for (int c = 0; c < 32; c++) m1 |= (uint32_t)((acc[c] >> (COMPACT ? 24 : 32)) == 1u) << c;
+        if (lane >= nw) m1 = 0;
+        uint32_t fpos;
+        {
+            const uint32_t n1 = __popc(m1);
+            uint32_t x = n1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+            uint32_t base = 0;
+            if (lane == 31 && tot) base = (uint32_t)atomicAdd(&ctrl->rc[0], (unsigned long long)tot);
+            fpos = __shfl_sync(0xffffffffu, base, 31) + x - n1;
+        }
         if (lane < nw) {
             const uint64_t e0 = (D << P.log2L) + 32 * lane;
             const float4* y4 = reinterpret_cast<const float4*>(counters + e0);
@@ -295,6 +316,10 @@ k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __rest
                 const float yv[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
+                    if ((m1 >> (4 * q + e)) & 1u)
+                        frontier[fpos++] = make_uint2((uint32_t)(e0 + 4 * q + e),
+                                                      COMPACT ? ((uint32_t)acc[4 * q + e] & 0xffffffu) | (j << 24)
+                                                              : (uint32_t)acc[4 * q + e]);
                     if (COMPACT) {
                         CellC st;
                         st.key = (uint32_t)acc[4 * q + e];
@@ -330,7 +355,7 @@ void launch_pair_lists(const KParams& P, const uint2* tabS, uint32_t* dst_off, u
 void launch_build_cells(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* gmask, uint32_t* dst_off, uint32_t* pair_pos,
                         uint32_t* dst_list, void* cells, Ctrl* ctrl, bool compact,
-                        cudaStream_t s) {
+                        uint2* frontier, cudaStream_t s) {
     const uint64_t nD = P.c >> P.log2L;
 #ifdef LHC_DEBUG_SYNC
 #define DBG(name) { cudaError_t e_ = cudaStreamSynchronize(s); if (e_) fprintf(stderr, "%s: %s\n", name, cudaGetErrorString(e_)); else fprintf(stderr, "%s ok\n", name); }
@@ -341,9 +366,11 @@ void launch_build_cells(const KParams& P, const float* counters, const uint2* ta
     DBG("pair_lists");
     const uint32_t gb = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((nD + 7) / 8, (uint64_t)num_sms() * 16));
     if (compact)
-        k_build_cells<true><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl);
+        k_build_cells<true><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl,
+                                               frontier);
     else
-        k_build_cells<false><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl);
+        k_build_cells<false><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl,
+                                                frontier);
     DBG("build_cells");
     count_launch(1);
 }
@@ -369,7 +396,8 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                           uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
                           uint8_t* __restrict__ out_peeled, lhc_stats* stats, uint64_t n_c,
                           const uint32_t* __restrict__ rowoff, uint2* vlog, uint32_t* vfill,
-                          uint2* sh_q, uint32_t* sh_n, uint32_t* sh_base, uint32_t* sh_peeled) {
+                          bool f0_done, uint2* sh_q, uint32_t* sh_n, uint32_t* sh_base,
+                          uint32_t* sh_peeled) {
     using C = Cells<COMPACT>;
     using Cell = typename C::T;
     using K = typename C::K;
@@ -383,7 +411,8 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
     const uint64_t pl = pol_last();
 
     // F0 ("round 0"): cells of degree one with their candidate, through rc[0]
-    {
+    // (already appended by the state build when the state was built by row)
+    if (!f0_done) {
         // four cells per thread and pass (four loads in flight); one global
         // reservation per buffer-full, not per pass
         const uint32_t qcap = kPeelThreads * peel_q_per_thread(k);  // entries of sh_q
@@ -644,7 +673,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
 // row, 2 = compact state prebuilt by destination row (falls back to mode 0 if the
 // build flagged a row with too many input rows).
 template <int KT>
-__global__ void __launch_bounds__(kPeelThreads, LHC_PEEL_MINB)
+__global__ void __launch_bounds__(kPeelThreads, KT ? LHC_PEEL_MINB : 1)
 k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
        const uint32_t* __restrict__ cand, float* dense, uint64_t cap, void* cells_v,
        uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* __restrict__ out_val,
@@ -687,6 +716,9 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     }
 
     if (mode == 0) {
+        // (a compact build that failed may have appended to the queue: start it over;
+        // nobody appends before the barriers below)
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->rc[0] = 0ull;
         CellState* cells = static_cast<CellState*>(cells_v);
         // cell state {key = 0, R = Y} (coalesced, 4 loads in flight per thread) ...
         uint64_t e = gtid;
@@ -727,12 +759,12 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     if (timer) ctrl->t[2] = globaltimer();
     if (mode == 2)
         peel_body<KT, true>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
-                            out_peeled, stats, n_c, rowoff, vlog, vfill, sh_q, &sh_n, &sh_base,
-                            &sh_peeled);
+                            out_peeled, stats, n_c, rowoff, vlog, vfill, true, sh_q, &sh_n,
+                            &sh_base, &sh_peeled);
     else
         peel_body<KT, false>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
-                             out_peeled, stats, n_c, rowoff, vlog, vfill, sh_q, &sh_n, &sh_base,
-                             &sh_peeled);
+                             out_peeled, stats, n_c, rowoff, vlog, vfill, mode == 1, sh_q, &sh_n,
+                             &sh_base, &sh_peeled);
 }
 
 constexpr uint64_t kSmallPeelCells = 1ull << 20;

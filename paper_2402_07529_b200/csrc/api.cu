@@ -369,10 +369,17 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
     // peel then runs only if a block could not be (mode 3: fallback, device-checked).
     int mode = p->c * sizeof(CellState) > (size_t)l2_bytes() / 2 ? 1 : 0;
     if (mode == 1 && v.P.nrows <= (1u << 22)) mode = 2;
+    // compact state beyond the L2: keys and residuals in two arrays, peeled in two
+    // passes that each keep half of it in L2 — when that half fits (VGG19: 1.74 ->
+    // 1.45 ms; LSTM, 118 MB of keys: 1.72 -> 1.98 ms) (LHC_PEEL_SPLIT=0/1 overrides)
+    bool split = p->c * sizeof(CellC) > (size_t)l2_bytes() / 2 &&
+                 p->c * sizeof(uint32_t) <= (size_t)l2_bytes() * 7 / 10;
+    if (const char* es = getenv("LHC_PEEL_SPLIT")) split = !strcmp(es, "1");
     bool blocked = peel_blocked_fits(v.P);
     if (const char* ev = getenv("LHC_CELL_BUILD")) {
         if (!strcmp(ev, "rows")) mode = 1, blocked = false;
-        if (!strcmp(ev, "compact")) mode = v.P.nrows <= (1u << 22) ? 2 : 1, blocked = false;
+        if (!strcmp(ev, "compact")) mode = v.P.nrows <= (1u << 22) ? 2 : 1, blocked = false, split = false;
+        if (!strcmp(ev, "split")) mode = v.P.nrows <= (1u << 22) ? 2 : 1, blocked = false, split = true;
         if (!strcmp(ev, "insert")) mode = 0, blocked = false;
     }
     // large blocks, one per thread-block cluster with the state in distributed shared
@@ -395,9 +402,10 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
         if (eb != cudaSuccess) return set_error(LHC_ECUDA, "blocked peel launch: %s", cudaGetErrorString(eb));
         mode = 3;
     }
-    if (mode == 1 || mode == 2)
+    if (mode == 2 && split) mode = 4;
+    if (mode == 1 || mode == 2 || mode == 4)
         launch_build_cells(v.P, counters, v.tabS, v.gmask, v.dst_off, v.pair_pos, v.dst_list,
-                           v.cells, v.ctrl, mode == 2, v.frontier, s);
+                           v.cells, v.ctrl, mode != 1, v.frontier, mode == 4, s);
     // the global peel writes every coordinate of the dense output itself (chunk by
     // chunk, after the rounds); with no dense output it writes only the list values
     cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, out_dense, cap_cand, v.cells, v.claim,

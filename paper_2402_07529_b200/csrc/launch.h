@@ -77,7 +77,7 @@ cudaError_t launch_peel_rows(const KParams& P, const float* counters, const uint
 void launch_build_cells(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* gmask, uint32_t* dst_off, uint32_t* pair_pos,
                         uint32_t* dst_list, void* cells, Ctrl* ctrl, bool compact,
-                        uint2* frontier, cudaStream_t s);
+                        uint2* frontier, bool split, cudaStream_t s);
 cudaError_t launch_peel(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* cand, float* dense, uint64_t cap, void* cells,
                         uint32_t* claim, uint2* frontier, Ctrl* ctrl, float* out_val,

@@ -227,7 +227,9 @@ __global__ void __launch_bounds__(256) k_pair_scatter(KParams P, const uint2* __
 #ifndef LHC_BUILD_MINB
 #define LHC_BUILD_MINB 3  // 80 registers: 3 CTAs of 256 per SM (VGG build 167 -> 140 us)
 #endif
-template <bool COMPACT>
+// SPLIT (compact only): keys and residuals in two arrays, keys = cells_v[0, c),
+// R = cells_v[c, 2c) as 4-byte words (the two-pass peel, peel_split).
+template <bool COMPACT, bool SPLIT>
 __global__ void __launch_bounds__(256, LHC_BUILD_MINB)
 k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
               const uint32_t* __restrict__ gmask, const uint32_t* __restrict__ dst_off,
@@ -307,7 +309,24 @@ k_build_cells(KParams P, const float* __restrict__ counters, const uint2* __rest
             if (lane == 31 && tot) base = (uint32_t)atomicAdd(&ctrl->rc[0], (unsigned long long)tot);
             fpos = __shfl_sync(0xffffffffu, base, 31) + x - n1;
         }
-        if (lane < nw) {
+        if (SPLIT && lane < nw) {
+            const uint64_t e0 = (D << P.log2L) + 32 * lane;
+            const float4* y4 = reinterpret_cast<const float4*>(counters + e0);
+            uint4* k4 = reinterpret_cast<uint4*>(static_cast<uint32_t*>(cells_v) + e0);
+            float4* r4 = reinterpret_cast<float4*>(static_cast<float*>(cells_v) + P.c + e0);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const float4 y = __ldcs(y4 + q);
+                r4[q] = y;
+                k4[q] = make_uint4((uint32_t)acc[4 * q], (uint32_t)acc[4 * q + 1], (uint32_t)acc[4 * q + 2],
+                                   (uint32_t)acc[4 * q + 3]);
+#pragma unroll
+                for (int e = 0; e < 4; e++)
+                    if ((m1 >> (4 * q + e)) & 1u)
+                        frontier[fpos++] = make_uint2((uint32_t)(e0 + 4 * q + e),
+                                                      ((uint32_t)acc[4 * q + e] & 0xffffffu) | (j << 24));
+            }
+        } else if (lane < nw) {
             const uint64_t e0 = (D << P.log2L) + 32 * lane;
             const float4* y4 = reinterpret_cast<const float4*>(counters + e0);
 #pragma unroll
@@ -355,7 +374,7 @@ void launch_pair_lists(const KParams& P, const uint2* tabS, uint32_t* dst_off, u
 void launch_build_cells(const KParams& P, const float* counters, const uint2* tabS,
                         const uint32_t* gmask, uint32_t* dst_off, uint32_t* pair_pos,
                         uint32_t* dst_list, void* cells, Ctrl* ctrl, bool compact,
-                        uint2* frontier, cudaStream_t s) {
+                        uint2* frontier, bool split, cudaStream_t s) {
     const uint64_t nD = P.c >> P.log2L;
 #ifdef LHC_DEBUG_SYNC
 #define DBG(name) { cudaError_t e_ = cudaStreamSynchronize(s); if (e_) fprintf(stderr, "%s: %s\n", name, cudaGetErrorString(e_)); else fprintf(stderr, "%s ok\n", name); }
@@ -365,12 +384,15 @@ void launch_build_cells(const KParams& P, const float* counters, const uint2* ta
     launch_pair_lists(P, tabS, dst_off, pair_pos, dst_list, s);
     DBG("pair_lists");
     const uint32_t gb = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((nD + 7) / 8, (uint64_t)num_sms() * 16));
-    if (compact)
-        k_build_cells<true><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl,
-                                               frontier);
+    if (compact && split)
+        k_build_cells<true, true><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells,
+                                                     ctrl, frontier);
+    else if (compact)
+        k_build_cells<true, false><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells,
+                                                      ctrl, frontier);
     else
-        k_build_cells<false><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells, ctrl,
-                                                frontier);
+        k_build_cells<false, false><<<gb, 256, 0, s>>>(P, counters, tabS, gmask, dst_off, dst_list, cells,
+                                                       ctrl, frontier);
     DBG("build_cells");
     count_launch(1);
 }
@@ -388,6 +410,127 @@ struct Cells {
     __device__ static uint32_t deg(K key) { return (uint32_t)(key >> kShift); }
     __device__ static uint32_t low(K key) { return (uint32_t)(key & (((K)1 << kShift) - 1)); }
 };
+
+// Finalize, a warp per 1024-coordinate chunk q with a 4 KB tile in shared memory
+// (the queue buffer is free now): the chunk's candidates hold slots [s0, s1) of the
+// list, its peeled values are log entries [s0, vfill[q]).  Unpeeled candidates take
+// the median over j of sign_j * R; R of cell e is Rb[e * RS].
+template <int KT, int RS>
+__device__ void finalize_chunks(const KParams& P, const uint2* __restrict__ tabS,
+                                const uint32_t* __restrict__ cand, float* dense, const float* Rb,
+                                float* __restrict__ out_val, uint8_t* __restrict__ out_peeled,
+                                uint64_t n_c, const uint32_t* __restrict__ rowoff, const uint2* vlog,
+                                const uint32_t* vfill, uint2* sh_q) {
+    constexpr uint32_t NJ = KT ? KT : kMaxK;
+    const uint32_t k = KT ? (uint32_t)KT : P.k;
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    {
+        const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+        float* tile = reinterpret_cast<float*>(sh_q) + wib * (kTile + 32);
+        uint32_t* pm = reinterpret_cast<uint32_t*>(tile + kTile);  // peeled bits of the chunk
+        const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
+        const uint32_t rsh = 10 - P.log2L;  // input rows per chunk = 2^rsh
+        const uint64_t gw = gtid >> 5, nwarps = gstride >> 5;
+        // the next chunk's bounds are loaded while this one is assembled; the first
+        // 128 log entries and 128 candidate slots of a chunk are loaded together
+        uint32_t n_s0 = 0, n_s1 = 0, n_f1 = 0;
+        if (gw < nchunks) {
+            n_s0 = __ldcg(rowoff + (gw << rsh));
+            n_s1 = gw + 1 < nchunks ? __ldcg(rowoff + ((gw + 1) << rsh)) : (uint32_t)n_c;
+            n_f1 = __ldcg(vfill + gw);
+        }
+        for (uint64_t q = gw; q < nchunks; q += nwarps) {
+            const uint32_t s0 = n_s0, s1 = n_s1, f1 = n_f1;
+            const uint64_t qn = q + nwarps;
+            if (qn < nchunks) {
+                n_s0 = __ldcg(rowoff + (qn << rsh));
+                n_s1 = qn + 1 < nchunks ? __ldcg(rowoff + ((qn + 1) << rsh)) : (uint32_t)n_c;
+                n_f1 = __ldcg(vfill + qn);
+            }
+            uint2 ent[4];
+            uint32_t pc[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t a = s0 + lane + 32 * u;
+                ent[u] = a < f1 ? __ldcs(vlog + a) : make_uint2(0u, 0u);
+                pc[u] = a < s1 ? __ldg(cand + a) : 0u;
+            }
+            float4* t4 = reinterpret_cast<float4*>(tile);
+#pragma unroll
+            for (int u = 0; u < 8; u++) t4[lane + 32 * u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            pm[lane] = 0u;
+            __syncwarp();
+            for (uint32_t a0 = s0;;) {
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (a0 + lane + 32 * u < f1) {
+                        const uint32_t off = ent[u].x & (kTile - 1);
+                        tile[off] = __uint_as_float(ent[u].y);
+                        atomicOr(pm + (off >> 5), 1u << (off & 31));
+                    }
+                a0 += 128;
+                if (a0 >= f1) break;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t a = a0 + lane + 32 * u;
+                    ent[u] = a < f1 ? __ldcs(vlog + a) : make_uint2(0u, 0u);
+                }
+            }
+            __syncwarp();
+            for (uint32_t a0 = s0;;) {
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t sl = a0 + lane + 32 * u;
+                    if (sl >= s1) continue;
+                    const uint32_t p = pc[u];
+                    const uint32_t off = p & (kTile - 1);
+                    const bool pe = (pm[off >> 5] >> (off & 31)) & 1u;
+                    float val;
+                    if (pe) {
+                        val = tile[off];
+                    } else {
+                        float v[NJ];
+                        for (uint32_t j = 0; j < k; j++) {
+                            uint32_t neg;
+                            const uint32_t e = cand_cell(P, tabS, p, j, &neg);
+                            v[j] = (neg ? -1.f : 1.f) * __ldcg(Rb + (uint64_t)e * RS);
+                        }
+                        for (uint32_t a = 1; a < k; a++) {  // insertion sort of <= 8 values
+                            float x = v[a];
+                            int b = (int)a - 1;
+                            while (b >= 0 && v[b] > x) { v[b + 1] = v[b]; b--; }
+                            v[b + 1] = x;
+                        }
+                        val = (k & 1) ? v[k / 2] : 0.5f * (v[k / 2 - 1] + v[k / 2]);
+                        tile[off] = val;
+                    }
+                    out_peeled[sl] = pe ? 1 : 0;
+                    out_val[sl] = val;
+                }
+                a0 += 128;
+                if (a0 >= s1) break;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t a = a0 + lane + 32 * u;
+                    pc[u] = a < s1 ? __ldg(cand + a) : 0u;
+                }
+            }
+            __syncwarp();
+            if (dense) {
+                const uint64_t c0 = q * kTile;
+                if (c0 + kTile <= P.d) {
+                    float4* o4 = reinterpret_cast<float4*>(dense + c0);
+#pragma unroll
+                    for (int u = 0; u < 8; u++) __stcs(o4 + lane + 32 * u, t4[lane + 32 * u]);
+                } else {
+                    for (uint32_t a = lane; c0 + a < P.d; a += 32) dense[c0 + a] = tile[a];
+                }
+            }
+            __syncwarp();  // the tile is read before the next chunk clears it
+        }
+    }
+}
 
 // F0, the synchronous rounds and the finalize, on either layout.
 template <int KT, bool COMPACT>
@@ -549,115 +692,9 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
     }
     if (timer) ctrl->t[kCtrlTimes - 1] = globaltimer();
 
-    // finalize, a warp per 1024-coordinate chunk q with a 4 KB tile in shared memory
-    // (the queue buffer is free now): the chunk's candidates hold slots [s0, s1) of the
-    // list, its peeled values are log entries [s0, vfill[q]).  Unpeeled candidates
-    // take the median over j of sign_j * R.
-    {
-        const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-        float* tile = reinterpret_cast<float*>(sh_q) + wib * (kTile + 32);
-        uint32_t* pm = reinterpret_cast<uint32_t*>(tile + kTile);  // peeled bits of the chunk
-        const uint64_t nchunks = ((uint64_t)P.d + kTile - 1) / kTile;
-        const uint32_t rsh = 10 - P.log2L;  // input rows per chunk = 2^rsh
-        const uint64_t gw = gtid >> 5, nwarps = gstride >> 5;
-        // the next chunk's bounds are loaded while this one is assembled; the first
-        // 128 log entries and 128 candidate slots of a chunk are loaded together
-        uint32_t n_s0 = 0, n_s1 = 0, n_f1 = 0;
-        if (gw < nchunks) {
-            n_s0 = __ldcg(rowoff + (gw << rsh));
-            n_s1 = gw + 1 < nchunks ? __ldcg(rowoff + ((gw + 1) << rsh)) : (uint32_t)n_c;
-            n_f1 = __ldcg(vfill + gw);
-        }
-        for (uint64_t q = gw; q < nchunks; q += nwarps) {
-            const uint32_t s0 = n_s0, s1 = n_s1, f1 = n_f1;
-            const uint64_t qn = q + nwarps;
-            if (qn < nchunks) {
-                n_s0 = __ldcg(rowoff + (qn << rsh));
-                n_s1 = qn + 1 < nchunks ? __ldcg(rowoff + ((qn + 1) << rsh)) : (uint32_t)n_c;
-                n_f1 = __ldcg(vfill + qn);
-            }
-            uint2 ent[4];
-            uint32_t pc[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const uint32_t a = s0 + lane + 32 * u;
-                ent[u] = a < f1 ? __ldcs(vlog + a) : make_uint2(0u, 0u);
-                pc[u] = a < s1 ? __ldg(cand + a) : 0u;
-            }
-            float4* t4 = reinterpret_cast<float4*>(tile);
-#pragma unroll
-            for (int u = 0; u < 8; u++) t4[lane + 32 * u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            pm[lane] = 0u;
-            __syncwarp();
-            for (uint32_t a0 = s0;;) {
-#pragma unroll
-                for (int u = 0; u < 4; u++)
-                    if (a0 + lane + 32 * u < f1) {
-                        const uint32_t off = ent[u].x & (kTile - 1);
-                        tile[off] = __uint_as_float(ent[u].y);
-                        atomicOr(pm + (off >> 5), 1u << (off & 31));
-                    }
-                a0 += 128;
-                if (a0 >= f1) break;
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const uint32_t a = a0 + lane + 32 * u;
-                    ent[u] = a < f1 ? __ldcs(vlog + a) : make_uint2(0u, 0u);
-                }
-            }
-            __syncwarp();
-            for (uint32_t a0 = s0;;) {
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const uint32_t sl = a0 + lane + 32 * u;
-                    if (sl >= s1) continue;
-                    const uint32_t p = pc[u];
-                    const uint32_t off = p & (kTile - 1);
-                    const bool pe = (pm[off >> 5] >> (off & 31)) & 1u;
-                    float val;
-                    if (pe) {
-                        val = tile[off];
-                    } else {
-                        float v[NJ];
-                        for (uint32_t j = 0; j < k; j++) {
-                            uint32_t neg;
-                            const uint32_t e = cand_cell(P, tabS, p, j, &neg);
-                            v[j] = (neg ? -1.f : 1.f) * __ldcg(&cells[e].R);
-                        }
-                        for (uint32_t a = 1; a < k; a++) {  // insertion sort of <= 8 values
-                            float x = v[a];
-                            int b = (int)a - 1;
-                            while (b >= 0 && v[b] > x) { v[b + 1] = v[b]; b--; }
-                            v[b + 1] = x;
-                        }
-                        val = (k & 1) ? v[k / 2] : 0.5f * (v[k / 2 - 1] + v[k / 2]);
-                        tile[off] = val;
-                    }
-                    out_peeled[sl] = pe ? 1 : 0;
-                    out_val[sl] = val;
-                }
-                a0 += 128;
-                if (a0 >= s1) break;
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const uint32_t a = a0 + lane + 32 * u;
-                    pc[u] = a < s1 ? __ldg(cand + a) : 0u;
-                }
-            }
-            __syncwarp();
-            if (dense) {
-                const uint64_t c0 = q * kTile;
-                if (c0 + kTile <= P.d) {
-                    float4* o4 = reinterpret_cast<float4*>(dense + c0);
-#pragma unroll
-                    for (int u = 0; u < 8; u++) __stcs(o4 + lane + 32 * u, t4[lane + 32 * u]);
-                } else {
-                    for (uint32_t a = lane; c0 + a < P.d; a += 32) dense[c0 + a] = tile[a];
-                }
-            }
-            __syncwarp();  // the tile is read before the next chunk clears it
-        }
-    }
+    finalize_chunks<KT, COMPACT ? 2 : 4>(P, tabS, cand, dense,
+                                         reinterpret_cast<const float*>(cells) + (COMPACT ? 1 : 2),
+                                         out_val, out_peeled, n_c, rowoff, vlog, vfill, sh_q);
     if (LHC_PEEL_TIMING && threadIdx.x == 0) atomicMax(&ctrl->t[1], globaltimer());
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         stats->n_peeled = n_peeled;
@@ -668,10 +705,167 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
     }
 }
 
+// Two-pass peel on the split compact state (keys[c], R[c]: 4 bytes each), used when
+// the 8-byte cell state does not fit in L2.  The set of candidates peeled in each
+// synchronous round depends only on the degrees, so
+//   pass 1  runs the rounds on the keys alone (claim, key deductions, frontier
+//           appends) and marks every entry whose claim succeeded (bit 31 of its id);
+//           the end of each round's segment is kept in rend[] (<= c segments: every
+//           cell enters the queue at most once and every segment is non-empty);
+//   pass 2  replays the segments in order on the residuals alone: a marked entry
+//           (e, i | j << 24) reads its value from its pure cell e and deducts it from
+//           the other cells of its candidate, one grid barrier per segment —
+//           all cells that fed a pure cell were peeled in earlier segments.
+// Each pass works on half the state (VGG19: 64 MB), which then stays in L2.
+template <int KT>
+__device__ void peel_split(const KParams& P, const uint2* __restrict__ tabS,
+                           const uint32_t* __restrict__ cand, float* dense, uint32_t* keys, float* R,
+                           uint32_t* rend, uint32_t* claim, uint2* frontier, Ctrl* ctrl,
+                           float* __restrict__ out_val, uint8_t* __restrict__ out_peeled,
+                           lhc_stats* stats, uint64_t n_c, const uint32_t* __restrict__ rowoff,
+                           uint2* vlog, uint32_t* vfill, uint2* sh_q, uint32_t* sh_n,
+                           uint32_t* sh_base, uint32_t* sh_peeled) {
+    using C = Cells<true>;
+    cg::grid_group grid = cg::this_grid();
+    constexpr uint32_t NJ = KT ? KT : kMaxK;
+    const uint32_t k = KT ? (uint32_t)KT : P.k;
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
+    const uint64_t pl = pol_last();
+    grid.sync();
+    if (timer) ctrl->t[3] = globaltimer();
+
+    // ---- pass 1: degrees only
+    uint32_t f_begin = 0;
+    uint32_t f_end = (uint32_t)*(volatile unsigned long long*)&ctrl->rc[0];
+    uint32_t n_peeled = 0, rounds = 0, nseg = 0;
+    for (uint32_t r = 1; f_begin < f_end; r++) {
+        unsigned long long* rc = &ctrl->rc[r % 3];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctrl->rc[(r + 1) % 3] = 0ull;
+            rend[r - 1] = f_end;  // segment r - 1 (0-based) is [rend[r - 2], rend[r - 1])
+            if (r < kCtrlTimes - 4) {
+                ctrl->t[r + 3] = globaltimer();
+                ctrl->fsize[r] = f_end - f_begin;
+            }
+        }
+        nseg = r;
+        for (uint64_t base = f_begin + blockIdx.x * (uint64_t)blockDim.x; base < f_end; base += gstride) {
+            const uint64_t f = base + threadIdx.x;
+            if (f < f_end) {
+                const uint2 ent = frontier[f];
+                const uint32_t e = ent.x, i = ent.y & 0xffffffu, jp = ent.y >> 24;
+                const uint2* row = tabS + (uint64_t)i * k;
+                uint2 mp[NJ];
+#pragma unroll
+                for (uint32_t j = 0; j < NJ; j++) {
+                    if (!KT && j >= k) break;
+                    mp[j] = ld_nc_u2(row + j);
+                }
+                uint32_t bj = 0;
+#pragma unroll
+                for (uint32_t j = 0; j < NJ; j++)
+                    if (j == jp) bj = map_bias(mp[j]);
+                const uint32_t t = ((e & (P.L - 1)) + P.L - bj) & (P.L - 1);
+                const uint32_t p = (i << P.log2L) + t;
+                const uint32_t bit = 1u << (p & 31);
+                const uint32_t old = atomicOr(claim + (p >> 5), bit);
+                if (!(old & bit)) {
+                    atomicAdd(sh_peeled, 1u);
+                    const uint32_t dec = 0u - C::one(i);
+                    uint32_t rest[NJ];
+#pragma unroll
+                    for (uint32_t j = 0; j < NJ; j++) {
+                        if (!KT && j >= k) break;
+                        if (j == jp) continue;
+                        const uint32_t ev = (mp[j].x << P.log2L) + ((t + map_bias(mp[j])) & (P.L - 1));
+                        rest[j] = atom_add_hint(keys + ev, dec, pl) + dec;
+                    }
+                    frontier[f].y = ent.y | 0x80000000u;  // won: replayed by pass 2
+#pragma unroll
+                    for (uint32_t j = 0; j < NJ; j++) {
+                        if (!KT && j >= k) break;
+                        if (j != jp && C::deg(rest[j]) == 1u)
+                            sh_q[atomicAdd(sh_n, 1u)] =
+                                make_uint2((mp[j].x << P.log2L) + ((t + map_bias(mp[j])) & (P.L - 1)),
+                                           C::low(rest[j]) | (j << 24));
+                    }
+                }
+            }
+            flush_queue(sh_q, sh_n, sh_base, frontier, f_end, rc);
+        }
+        if (threadIdx.x == 0 && *sh_peeled) {
+            atomicAdd(rc, (unsigned long long)*sh_peeled << 32);
+            *sh_peeled = 0;
+        }
+        grid.sync();
+        const unsigned long long rcv = *(volatile unsigned long long*)rc;
+        const uint32_t np = (uint32_t)(rcv >> 32);
+        f_begin = f_end;
+        f_end += (uint32_t)rcv;
+        n_peeled += np;
+        if (np) rounds++;
+    }
+    if (timer) ctrl->t[kCtrlTimes - 2] = globaltimer();
+
+    // ---- pass 2: values, segment by segment (rend[] and the marks are ordered by the
+    // last barrier of pass 1)
+    for (uint32_t sgi = 0; sgi < nseg; sgi++) {
+        const uint32_t b = sgi ? __ldcg(rend + sgi - 1) : 0u, en = __ldcg(rend + sgi);
+        for (uint64_t f = b + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < en; f += gstride) {
+            const uint2 ent = __ldcs(frontier + f);
+            if (!(ent.y >> 31)) continue;
+            const uint32_t e = ent.x, i = ent.y & 0xffffffu, jp = (ent.y >> 24) & 0x7fu;
+            const float Re = ld_cg_f32(R + e);
+            const uint2* row = tabS + (uint64_t)i * k;
+            uint2 mp[NJ];
+#pragma unroll
+            for (uint32_t j = 0; j < NJ; j++) {
+                if (!KT && j >= k) break;
+                mp[j] = ld_nc_u2(row + j);
+            }
+            uint32_t bj = 0;
+            float ge = 1.f;
+#pragma unroll
+            for (uint32_t j = 0; j < NJ; j++)
+                if (j == jp) { bj = map_bias(mp[j]); ge = map_sign(mp[j]); }
+            const uint32_t t = ((e & (P.L - 1)) + P.L - bj) & (P.L - 1);
+            const uint32_t p = (i << P.log2L) + t;
+            const float val = ge * Re;
+            const uint32_t q = p >> 10, lane = threadIdx.x & 31;
+            const uint32_t peers = __match_any_sync(__activemask(), q);
+            const uint32_t leader = __ffs(peers) - 1;
+            uint32_t lbase = 0;
+            if (lane == leader) lbase = atomicAdd(vfill + q, (uint32_t)__popc(peers));
+#pragma unroll
+            for (uint32_t j = 0; j < NJ; j++) {
+                if (!KT && j >= k) break;
+                if (j == jp) continue;
+                red_add_hint(R + (mp[j].x << P.log2L) + ((t + map_bias(mp[j])) & (P.L - 1)),
+                             -map_sign(mp[j]) * val, pl);
+            }
+            lbase = __shfl_sync(peers, lbase, leader) + __popc(peers & ((1u << lane) - 1u));
+            vlog[lbase] = make_uint2(p, __float_as_uint(val));
+        }
+        grid.sync();
+    }
+    if (timer) ctrl->t[kCtrlTimes - 1] = globaltimer();
+    finalize_chunks<KT, 1>(P, tabS, cand, dense, R, out_val, out_peeled, n_c, rowoff, vlog, vfill, sh_q);
+    if (LHC_PEEL_TIMING && threadIdx.x == 0) atomicMax(&ctrl->t[1], globaltimer());
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        stats->n_peeled = n_peeled;
+        stats->rounds = rounds;
+        stats->success = (uint64_t)n_peeled == n_c ? 1 : 0;
+        stats->entries = f_end;
+        ctrl->rounds_dbg = rounds;
+    }
+}
+
 // KT: compile-time k (3) or 0 for a run-time k <= kMaxK.  mode: 0 = build the wide
 // state here (per-candidate reductions), 1 = wide state prebuilt by destination
 // row, 2 = compact state prebuilt by destination row (falls back to mode 0 if the
-// build flagged a row with too many input rows).
+// build flagged a row with too many input rows), 4 = the same state split into key
+// and residual arrays, peeled in two passes (peel_split; same fallback).
 template <int KT>
 __global__ void __launch_bounds__(kPeelThreads, KT ? LHC_PEEL_MINB : 1)
 k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ tabS,
@@ -701,7 +895,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
     if (threadIdx.x == 0) { sh_n = 0; sh_peeled = 0; }
     if (timer) ctrl->t[0] = globaltimer();
-    if (mode == 2 && *(volatile uint32_t*)&ctrl->compact_fail) mode = 0;  // uniform
+    if ((mode == 2 || mode == 4) && *(volatile uint32_t*)&ctrl->compact_fail) mode = 0;  // uniform
     if (mode == 3) {  // fallback after the blocked peel: only if a block could not be peeled
         if (!*(volatile uint32_t*)&ctrl->blk_fail) return;
         mode = 0;
@@ -757,7 +951,12 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
         grid.sync();
     }
     if (timer) ctrl->t[2] = globaltimer();
-    if (mode == 2)
+    if (mode == 4)
+        peel_split<KT>(P, tabS, cand, dense, static_cast<uint32_t*>(cells_v),
+                       static_cast<float*>(cells_v) + P.c, static_cast<uint32_t*>(cells_v) + 2 * P.c,
+                       claim, frontier, ctrl, out_val, out_peeled, stats, n_c, rowoff, vlog, vfill, sh_q,
+                       &sh_n, &sh_base, &sh_peeled);
+    else if (mode == 2)
         peel_body<KT, true>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
                             out_peeled, stats, n_c, rowoff, vlog, vfill, true, sh_q, &sh_n,
                             &sh_base, &sh_peeled);

@@ -307,7 +307,7 @@ def test_pipeline(lhc, ora, d, nnz, W, L, structure, law):
         assert np.array_equal(F(dec.dense), np.sum(np.stack(xs).astype(np.float64), axis=0))
 
 
-@pytest.mark.parametrize("build", ["rows", "compact", "insert"])
+@pytest.mark.parametrize("build", ["rows", "compact", "split", "insert"])
 @pytest.mark.parametrize("d,nnz,W,L,structure", CASES)
 def test_cell_build_paths(lhc, ora, d, nnz, W, L, structure, build, monkeypatch):
     """Both ways of building the peeling state (per-candidate reductions, or by
@@ -324,9 +324,13 @@ def test_cell_build_paths(lhc, ora, d, nnz, W, L, structure, build, monkeypatch)
     compare_decode(ora, dec, ref, exact=True)
 
 
+@pytest.mark.parametrize("build", ["default", "split"])
 @pytest.mark.parametrize("gamma", [0.9, 1.1, 1.2, 1.25, 1.5])
-def test_decode_threshold_sweep(lhc, ora, gamma):
+def test_decode_threshold_sweep(lhc, ora, gamma, build, monkeypatch):
     # near and below the peeling threshold: flags, rounds and the median fallback
+    # (also through the two-pass peel of the split state)
+    if build != "default":
+        monkeypatch.setenv("LHC_CELL_BUILD", build)
     d, L, n = 2_000_000, 1024, 40_000
     rng = rng_for(int(gamma * 100))
     idx = support(rng, d, n)

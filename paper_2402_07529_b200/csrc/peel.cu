@@ -812,6 +812,7 @@ __device__ void peel_split(const KParams& P, const uint2* __restrict__ tabS,
     // last barrier of pass 1)
     for (uint32_t sgi = 0; sgi < nseg; sgi++) {
         const uint32_t b = sgi ? __ldcg(rend + sgi - 1) : 0u, en = __ldcg(rend + sgi);
+        if (LHC_PEEL_TIMING && timer && sgi < kCtrlTimes) ctrl->tflush[sgi] = globaltimer();
         for (uint64_t f = b + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < en; f += gstride) {
             const uint2 ent = __ldcs(frontier + f);
             if (!(ent.y >> 31)) continue;

@@ -39,9 +39,16 @@ def main():
         for r in range(1, 100):
             if not t[r + 3]:
                 break
-            nxt = t[r + 4] if t[r + 4] else t[127]
+            nxt = t[r + 4] if t[r + 4] else (t[126] if t[126] else t[127])
             rows.append(f"{r}:{fs[r]}/{(nxt - t[r + 3]) / 1e3:.1f}us")
         print("   round:entries/time", " ".join(rows))
+        if t[126]:  # two-pass peel: t[126] = end of pass 1, t[127] = end of pass 2
+            print(f"   pass 1 {(t[126] - t[3]) / 1e3:.1f} us, pass 2 {(t[127] - t[126]) / 1e3:.1f} us")
+            o2 = off_t + 128 * 8 + 512 + 1024  # Ctrl.tflush: pass-2 segment starts
+            tf = np.frombuffer(raw[o2:o2 + 1024], dtype=np.uint64).astype(np.int64)
+            n = int(np.count_nonzero(tf))
+            seg = [(tf[s + 1] if s + 1 < n else t[127]) - tf[s] for s in range(n)]
+            print("   pass 2 segment times (us):", " ".join(f"{x / 1e3:.1f}" for x in seg))
 
 
 if __name__ == "__main__":

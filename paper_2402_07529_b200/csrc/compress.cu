@@ -1,6 +1,9 @@
 // compress.cu — Phase I of Alg. 1 on sm_100a: hash kernel, dense and
 // COO compression into the Bloom filter B and the Count Sketch Y
 // in the batched, rotated layout of §3.4.
+#include <cstdlib>
+#include <cstring>
+
 #include "launch.h"
 
 namespace lhc {
@@ -291,25 +294,210 @@ k_compress_dense(KParams P, const __grid_constant__ CompressBatch B,
     }
 }
 
+// Row-major order (the default): a warp takes chunk r of every input of the batch in
+// turn (input b fastest), so the chunk's row maps — which depend only on the row
+// — are hashed once for the n inputs, and the n inputs' reductions into the
+// same destination rows follow each other.  KT / KBT: compile-time k and k_bloom (3),
+// or 0 for run-time values.  The chunk's nonzeros are compacted (ascending
+// coordinates in shared memory) before the Count Sketch reductions, one nonzero per
+// lane: lane-serial over each lane's word when the words are sparse, warp-cooperative
+// over the nonzero words when a few are dense.
+template <int KT, int KBT>
+__global__ void __launch_bounds__(kCompressThreads)
+k_compress_rows(KParams P, const __grid_constant__ CompressBatch B, uint64_t nrc,
+                unsigned long long* __restrict__ nnz_out) {
+    extern __shared__ __align__(128) unsigned char sh_all[];
+    constexpr uint32_t NK = KT ? KT : kMaxK, NKB = KBT ? KBT : kMaxK;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t k = KT ? (uint32_t)KT : P.k, kb = KBT ? (uint32_t)KBT : P.kb;
+    const uint32_t kk = k + kb;
+    const uint32_t n_map = (kTile >> P.log2L) * kk;  // row maps per chunk
+    unsigned char* mine = sh_all + warp * compress_warp_smem(n_map);
+    float* sh_x = reinterpret_cast<float*>(mine);  // [kStages][kTile]
+    uint16_t* sh_pos = reinterpret_cast<uint16_t*>(sh_x + kStages * kTile);
+    uint2* sh_map = reinterpret_cast<uint2*>(sh_pos + kTile);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sh_map) +
+                                                ((n_map * 8 + 15) / 16) * 16);
+    const uint32_t n = B.n;
+    const uint64_t stride = (uint64_t)gridDim.x * kCompressWarps;
+    const uint64_t first = blockIdx.x * (uint64_t)kCompressWarps + warp;
+    uint64_t pol_keep, pol_stream;
+    {
+        uint64_t pol_norm;
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_norm));
+        pol_keep = (LHC_COMPRESS_POL & 1) ? pol_norm : policy_evict_last();
+        pol_stream = (LHC_COMPRESS_POL & 2) ? pol_norm : policy_evict_first();
+    }
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t my_nnz = 0;
+
+    if (lane == 0) {
+        for (int st = 0; st < kStages; st++) mbar_init(bar + st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // prefetch cursor (lane 0): unit (pr, pb) goes to the stage after the last one;
+    // whole chunks are bulk-copied, a ragged last chunk is loaded plainly when used
+    uint64_t pr = first;
+    uint32_t pb = 0;
+    auto issue = [&](uint32_t sa, bool fence) {
+        if (pr < nrc && pr < B.d[pb] / kTile) {
+            if (fence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(sh_x + sa * kTile, B.x[pb] + pr * kTile, kTile * 4, bar + sa, pol_stream);
+        }
+        if (++pb == n) { pb = 0; pr += stride; }
+    };
+    if (lane == 0)
+        for (int st = 0; st < kStages - 1; st++) issue((uint32_t)st, false);
+    uint64_t cr = first;
+    uint32_t cb = 0, it = 0, phase = 0;
+    while (cr < nrc) {
+        const uint32_t st = it % kStages;
+        if (lane == 0) issue((it + kStages - 1) % kStages, true);
+        if (cb == 0) {  // a new chunk row: its maps (the previous unit's readers are done)
+            const uint64_t row0 = cr << (10 - P.log2L);
+            for (uint32_t a = lane; a < n_map; a += 32) {
+                const uint32_t r = a / kk, jj = a - r * kk;
+                sh_map[a] = jj < k ? dom_map(P, 0, jj, row0 + r) : dom_map(P, 1, jj - k, row0 + r);
+            }
+        }
+        const uint32_t d_in = B.d[cb];
+        const uint64_t base = cr * kTile;
+        float* cx = sh_x + st * kTile;
+        const bool live = base < d_in;
+        if (live) {
+            if (cr < d_in / kTile) {
+                mbar_wait(bar + st, (phase >> st) & 1u);
+                phase ^= 1u << st;
+            } else {  // ragged last chunk: plain loads
+                const float* x = B.x[cb];
+                for (uint32_t a = lane; a < kTile; a += 32) cx[a] = base + a < d_in ? x[base + a] : 0.f;
+            }
+        }
+        __syncwarp();
+        if (live) {
+            // nonzero words: lane w builds word w from its 32 values (eight 16-byte
+            // shared loads, rotated by w so a quarter-warp hits distinct banks)
+            uint32_t word = 0;
+            {
+                const float4* cw = reinterpret_cast<const float4*>(cx + 32 * lane);
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const uint32_t qq = (q + lane) & 7;
+                    const float4 v = cw[qq];
+                    const uint32_t nib = (v.x != 0.f ? 1u : 0u) | (v.y != 0.f ? 2u : 0u) |
+                                         (v.z != 0.f ? 4u : 0u) | (v.w != 0.f ? 8u : 0u);
+                    word |= nib << (4 * qq);
+                }
+            }
+            const uint32_t nzw = __ballot_sync(kFullMask, word != 0);
+            const uint32_t pc = __popc(word);
+            my_nnz += pc;
+            if (nzw) {  // uniform
+                uint32_t* __restrict__ bitmap = B.bitmap[cb];
+                float* __restrict__ counters = B.counters[cb];
+                // Bloom filter, lane w = word w of the chunk
+                const uint32_t r = lane >> P.log2nw, w = lane & (P.nw - 1);
+                const uint32_t seg = r << P.log2nw;
+#pragma unroll
+                for (uint32_t j = 0; j < NKB; j++) {
+                    if (!KBT && j >= kb) break;
+                    const uint2 mp = sh_map[r * kk + k + j];
+                    const uint32_t sb = (32 * w + P.L - map_bias(mp)) & (P.L - 1);  // (32w - bias) mod L
+                    const uint32_t sw = sb >> 5, sh = sb & 31;
+                    const uint32_t lo = __shfl_sync(kFullMask, word, seg + sw);
+                    const uint32_t hi = __shfl_sync(kFullMask, word, seg + ((sw + 1) & (P.nw - 1)));
+                    const uint32_t dst = __funnelshift_r(lo, hi, sh);
+                    if (dst) red_or(bitmap + (uint64_t)mp.x * P.nw + w, dst, pol_keep);
+                }
+                // compaction of the chunk's nonzero coordinates
+                uint32_t total;
+                if (__reduce_max_sync(kFullMask, pc) <= (uint32_t)__popc(nzw)) {
+                    uint32_t x = pc;  // inclusive warp scan of the counts
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+                        if (lane >= (uint32_t)o) x += y;
+                    }
+                    total = __shfl_sync(kFullMask, x, 31);
+                    uint32_t off = x - pc;
+                    for (uint32_t mm = word; mm; mm &= mm - 1) sh_pos[off++] = (uint16_t)(32 * lane + (__ffs(mm) - 1));
+                } else {
+                    total = 0;
+                    for (uint32_t z = nzw; z; z &= z - 1) {
+                        const uint32_t wz = __ffs(z) - 1;
+                        const uint32_t mw = __shfl_sync(kFullMask, word, wz);
+                        if (mw & (1u << lane)) sh_pos[total + __popc(mw & lt)] = (uint16_t)(32 * wz + lane);
+                        total += __popc(mw);
+                    }
+                }
+                __syncwarp();
+                // Count Sketch: one nonzero per lane, sign_j * x into each of its k cells
+                for (uint32_t a = lane; a < total; a += 32) {
+                    const uint32_t c0 = sh_pos[a];
+                    const float v = cx[c0];
+                    const uint32_t rr = c0 >> P.log2L, t = c0 & (P.L - 1);
+#pragma unroll
+                    for (uint32_t j = 0; j < NK; j++) {
+                        if (!KT && j >= k) break;
+                        const uint2 mp = sh_map[rr * kk + j];
+                        red_add(counters + ((uint64_t)mp.x << P.log2L) + ((t + map_bias(mp)) & (P.L - 1)),
+                                map_sign(mp) * v, pol_keep);
+                    }
+                }
+            }
+        }
+        __syncwarp();  // the stage buffer, the positions and the maps are rewritten next
+        it++;
+        if (++cb == n) { cb = 0; cr += stride; }
+    }
+    if (nnz_out) {
+        for (int o = 16; o; o >>= 1) my_nnz += __shfl_xor_sync(kFullMask, my_nnz, o);
+        if (lane == 0 && my_nnz) atomicAdd(nnz_out, (unsigned long long)my_nnz);
+    }
+}
+
 void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned long long* nnz_out,
                            cudaStream_t s) {
     const uint64_t nchunks = B.start[B.n];
     const uint32_t n_map = (kTile >> P.log2L) * (P.k + P.kb);
     const size_t smem = kCompressWarps * compress_warp_smem(n_map);
-    static int per_sm[64][6] = {};
+    const size_t smax = kCompressWarps * compress_warp_smem(32 * 2 * kMaxK);
+    // (LHC_COMPRESS_IMPL=chunks: the input-major kernel, one chunk of one input per unit)
+    static const bool by_chunks = [] {
+        const char* e = getenv("LHC_COMPRESS_IMPL");
+        return e && !strcmp(e, "chunks");
+    }();
+    const bool fast = P.k == 3 && P.kb == 3;
+    const void* fn = by_chunks ? (const void*)k_compress_dense
+                     : fast    ? (const void*)k_compress_rows<3, 3>
+                               : (const void*)k_compress_rows<0, 0>;
+    const int fi = by_chunks ? 0 : fast ? 1 : 2;
+    static int per_sm[64][3][6] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     const int key = 10 - (int)P.log2L > 5 ? 5 : 10 - (int)P.log2L;
-    if (dev < 64 && !per_sm[dev][key]) {
-        const size_t smax = kCompressWarps * compress_warp_smem(32 * 2 * kMaxK);
-        cudaFuncSetAttribute(k_compress_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
-        int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_compress_dense, kCompressThreads, smem);
-        per_sm[dev][key] = std::max(1, n);
+    if (dev < 64 && !per_sm[dev][fi][key]) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kCompressThreads, smem);
+        per_sm[dev][fi][key] = std::max(1, nb);
     }
-    const uint32_t blocks = (uint32_t)std::min<uint64_t>((nchunks + kCompressWarps - 1) / kCompressWarps,
-                                                         (uint64_t)num_sms() * (dev < 64 ? per_sm[dev][key] : 2));
-    k_compress_dense<<<blocks, kCompressThreads, smem, s>>>(P, B, nnz_out);
+    const int resident = dev < 64 ? per_sm[dev][fi][key] : 2;
+    if (by_chunks) {
+        const uint32_t blocks = (uint32_t)std::min<uint64_t>((nchunks + kCompressWarps - 1) / kCompressWarps,
+                                                             (uint64_t)num_sms() * resident);
+        k_compress_dense<<<blocks, kCompressThreads, smem, s>>>(P, B, nnz_out);
+    } else {
+        uint64_t nrc = 0;  // chunk rows: the longest input's chunks
+        for (uint32_t b = 0; b < B.n; b++) nrc = std::max<uint64_t>(nrc, B.start[b + 1] - B.start[b]);
+        const uint32_t blocks = (uint32_t)std::min<uint64_t>((nrc + kCompressWarps - 1) / kCompressWarps,
+                                                             (uint64_t)num_sms() * resident);
+        if (fast)
+            k_compress_rows<3, 3><<<blocks, kCompressThreads, smem, s>>>(P, B, nrc, nnz_out);
+        else
+            k_compress_rows<0, 0><<<blocks, kCompressThreads, smem, s>>>(P, B, nrc, nnz_out);
+    }
     count_launch();
 }
 

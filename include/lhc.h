@@ -313,6 +313,16 @@ int sketch_decompress_det(const lhc_params* p, const uint32_t* bitmap, const flo
  * on this thread (bench accounting of `gpu_launches`). */
 int lhc_last_launch_count(void);
 
+/* Reserve `fraction` (0..1) of the current device's maximum persisting-L2 set-aside
+ * (cudaLimitPersistingL2CacheSize; a device-wide setting of the calling process).
+ * The kernels mark the lines they reuse with L2 evict-last hints (the sketch during
+ * the compress, "random memory access lead to frequent cache misses"; the
+ * decode state during the peel); those hints only protect lines inside this
+ * set-aside, which is 0 by default.  *set_bytes (may be NULL) receives the bytes
+ * reserved.  LHC_EINVAL for a fraction outside [0, 1]; LHC_ECUDA if the runtime
+ * refuses the limit. */
+int lhc_l2_persist(double fraction, size_t* set_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,7 @@ EXPORTS = [
     "sketch_reduce_scatter", "sketch_allgather_decoded", "sketch_compress_batch",
     "sketch_clear_batch", "lhc_nvls_open", "lhc_nvls_bind", "sketch_allreduce_nvls",
     "sketch_reduce_scatter_nvls", "sketch_allgather_decoded_nvls", "lhc_nvls_destroy",
+    "lhc_l2_persist",
 ]
 
 
@@ -132,6 +133,7 @@ def lib() -> ctypes.CDLL:
             "sketch_reduce_scatter_nvls": (i32, [vp, P, u64, vp]),
             "sketch_allgather_decoded_nvls": (i32, [vp, P, u64, vp, vp, vp, u64, u32, vp, vp]),
             "lhc_nvls_destroy": (None, [vp]),
+            "lhc_l2_persist": (i32, [ctypes.c_double, ctypes.POINTER(sz)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -147,6 +149,14 @@ def last_error() -> str:
 
 def last_launch_count() -> int:
     return int(lib().lhc_last_launch_count())
+
+
+def l2_persist(fraction: float = 1.0) -> int:
+    """Reserve `fraction` of the device's persisting-L2 set-aside, which the kernels'
+    evict-last hints need to take effect (lhc_l2_persist); returns the bytes set."""
+    out = ctypes.c_size_t(0)
+    _check("lhc_l2_persist", lib().lhc_l2_persist(float(fraction), ctypes.byref(out)))
+    return int(out.value)
 
 
 def _check(fn: str, rc: int):

@@ -126,4 +126,23 @@ void launch_clear(int n, uint32_t* const* bitmaps, uint64_t n_words, float* cons
     }
 }
 
+// Demote the lines of [p, p + bytes) to the normal L2 eviction priority.  Lines
+// written or reduced with evict-last hints stay in the persisting-L2 set-aside
+// (lhc_l2_persist) until demoted: the compress pins the sketch, the decode demotes
+// it first so that its own working set gets the whole L2.
+__global__ void __launch_bounds__(256) k_l2_demote(const char* p, uint64_t lines) {
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < lines;
+         u += (uint64_t)gridDim.x * blockDim.x)
+        asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(p + u * 128) : "memory");
+}
+
+void launch_l2_demote(const void* p, size_t bytes, cudaStream_t s) {
+    if (!p || !bytes) return;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(127);
+    const uint64_t lines = (reinterpret_cast<uintptr_t>(p) + bytes - a0 + 127) / 128;
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((lines + 255) / 256, (uint64_t)num_sms() * 8);
+    k_l2_demote<<<blocks, 256, 0, s>>>(reinterpret_cast<const char*>(a0), lines);
+    count_launch();
+}
+
 }  // namespace lhc

@@ -153,6 +153,24 @@ const char* lhc_last_error(void) { return g_err; }
 
 int lhc_last_launch_count(void) { return g_launches; }
 
+// set by lhc_l2_persist: evict-last lines stay pinned in the set-aside, so the decode
+// demotes the sketch (and its own state when it is done)
+static bool g_l2_persist = false;
+
+int lhc_l2_persist(double fraction, size_t* set_bytes) {
+    if (!(fraction >= 0.0 && fraction <= 1.0)) return set_error(LHC_EINVAL, "fraction outside [0, 1]");
+    int dev = 0, mx = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess)
+        return set_error(LHC_ECUDA, "persisting L2 attribute: %s", cudaGetErrorString(cudaGetLastError()));
+    const size_t bytes = (size_t)((double)mx * fraction);
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess)
+        return set_error(LHC_ECUDA, "persisting L2 limit: %s", cudaGetErrorString(cudaGetLastError()));
+    if (set_bytes) *set_bytes = bytes;
+    g_l2_persist = bytes > 0;
+    return LHC_OK;
+}
+
 uint64_t lhc_bitmap_words(const lhc_params* p) { return validate(p) ? 0 : p->m / 32; }
 
 size_t lhc_decompress_workspace(const lhc_params* p, uint64_t cap_cand) {
@@ -343,6 +361,7 @@ int sketch_query(const lhc_params* p, const uint32_t* bitmap, void* ws, size_t w
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaMemsetAsync(v.ctrl, 0, sizeof(Ctrl), s) != cudaSuccess) return check_launch("memset");
     if (cudaMemsetAsync(stats, 0, sizeof(lhc_stats), s) != cudaSuccess) return check_launch("memset");
+    if (g_l2_persist) launch_l2_demote(bitmap, v.P.m / 8, s);
     cudaError_t e = launch_query(v.P, bitmap, v.tabS, v.gmask, v.cta_total, cap_cand, out_idx,
                                  v.ctrl, stats, v.rowoff, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "query launch: %s", cudaGetErrorString(e));
@@ -408,10 +427,15 @@ int sketch_peel(const lhc_params* p, const float* counters, void* ws, size_t ws_
                            v.cells, v.ctrl, mode != 1, v.frontier, mode == 4, s);
     // the global peel writes every coordinate of the dense output itself (chunk by
     // chunk, after the rounds); with no dense output it writes only the list values
+    if (g_l2_persist) launch_l2_demote(counters, v.P.c * sizeof(float), s);
     cudaError_t e = launch_peel(v.P, counters, v.tabS, out_idx, out_dense, cap_cand, v.cells, v.claim,
                                 v.frontier, v.ctrl, out_val, out_peeled, stats, v.rowoff, v.vlog,
                                 v.vfill, mode, s);
     if (e != cudaSuccess) return set_error(LHC_ECUDA, "peel launch: %s", cudaGetErrorString(e));
+    if (g_l2_persist) {  // the peel's evict-last state
+        launch_l2_demote(v.cells, v.P.c * (mode == 2 || mode == 4 ? sizeof(CellC) : sizeof(CellState)), s);
+        launch_l2_demote(v.claim, ((size_t)v.P.d + 7) / 8, s);
+    }
     return check_launch("sketch_peel");
 }
 

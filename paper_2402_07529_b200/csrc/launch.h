@@ -33,6 +33,7 @@ struct CompressBatch {
     // row) hit each sketch line while it is in L2
     uint32_t interleave;
 };
+void launch_l2_demote(const void* p, size_t bytes, cudaStream_t s);
 void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned long long* nnz_out,
                            cudaStream_t s);
 void launch_compress_coo(const KParams& P, uint64_t nnz, const uint32_t* idx, const float* val,

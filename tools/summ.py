@@ -11,4 +11,4 @@ for f in sys.argv[1:]:
     k = d.get("kernels", {})
     print(f"{f:40s} {d['config']['workload']:5s} {d['ms_per_step']:.3f} ms {d['value']:.3g} "
           + " ".join(f"{n}={v['us_per_step']:.0f}" for n, v in k.items())
-          + f" frac={d['roofline']['frac']:.3f}")
+          + f" frac={d.get('roofline', {}).get('frac', float('nan')):.3f}")

@@ -192,6 +192,52 @@ __device__ __forceinline__ void flush_queue(uint2* sh_q, uint32_t* sh_n, uint32_
     __syncthreads();
 }
 
+// Warp-private append buffers (kWarpQ entries of the shared queue buffer per warp):
+// the warps of a CTA append without block barriers; a full buffer is flushed by its
+// warp alone (one global reservation), the rest once per round by the CTA (one
+// reservation for all its warps, with the round's peel count in the high half).
+constexpr uint32_t kWarpQ = 512;
+__device__ __forceinline__ void wq_push(bool has, uint2 v, uint2* wbuf, uint32_t& wn, uint2* frontier,
+                                        uint32_t seg_base, unsigned long long* rc) {
+    const uint32_t lane = threadIdx.x & 31;
+    if (wn + 32 > kWarpQ) {  // warp-uniform
+        __syncwarp();
+        uint32_t b = 0;
+        if (lane == 0) b = (uint32_t)atomicAdd(rc, (unsigned long long)wn);
+        b = __shfl_sync(0xffffffffu, b, 0) + seg_base;
+        for (uint32_t a = lane; a < wn; a += 32) frontier[b + a] = wbuf[a];
+        __syncwarp();
+        wn = 0;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, has);
+    if (has) wbuf[wn + __popc(m & ((1u << lane) - 1u))] = v;
+    wn += __popc(m);
+}
+// End of a round: every warp's remaining entries, one reservation per CTA.
+__device__ __forceinline__ void wq_round_end(uint2* wbuf, uint32_t& wn, uint32_t& wpeel, uint32_t* sh_wc,
+                                             uint32_t* sh_wp, uint32_t* sh_base, uint2* frontier,
+                                             uint32_t seg_base, unsigned long long* rc) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    __syncwarp();
+    if (lane == 0) { sh_wc[warp] = wn; sh_wp[warp] = wpeel; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0, pe = 0;
+        for (uint32_t w = 0; w < nwarps; w++) {
+            const uint32_t c = sh_wc[w];
+            sh_wc[w] = tot;
+            tot += c;
+            pe += sh_wp[w];
+        }
+        *sh_base = tot || pe ? seg_base + (uint32_t)atomicAdd(rc, ((unsigned long long)pe << 32) + tot) : 0u;
+    }
+    __syncthreads();
+    const uint32_t b = *sh_base + sh_wc[warp];
+    for (uint32_t a = lane; a < wn; a += 32) frontier[b + a] = wbuf[a];
+    wn = 0;
+    wpeel = 0;
+}
+
 // ---- cell state by destination row, without atomics on cells ---------------------
 // (used when the cell state, 16 B per cell, does not fit in L2: then the
 // per-candidate 64-bit reductions of the in-kernel insert go to HBM at random)
@@ -723,8 +769,8 @@ __device__ void peel_split(const KParams& P, const uint2* __restrict__ tabS,
                            uint32_t* rend, uint32_t* claim, uint2* frontier, Ctrl* ctrl,
                            float* __restrict__ out_val, uint8_t* __restrict__ out_peeled,
                            lhc_stats* stats, uint64_t n_c, const uint32_t* __restrict__ rowoff,
-                           uint2* vlog, uint32_t* vfill, uint2* sh_q, uint32_t* sh_n,
-                           uint32_t* sh_base, uint32_t* sh_peeled) {
+                           uint2* vlog, uint32_t* vfill, uint2* sh_q, uint32_t* sh_wc,
+                           uint32_t* sh_wp, uint32_t* sh_base) {
     using C = Cells<true>;
     cg::grid_group grid = cg::this_grid();
     constexpr uint32_t NJ = KT ? KT : kMaxK;
@@ -736,6 +782,8 @@ __device__ void peel_split(const KParams& P, const uint2* __restrict__ tabS,
     if (timer) ctrl->t[3] = globaltimer();
 
     // ---- pass 1: degrees only
+    uint2* wbuf = sh_q + (threadIdx.x >> 5) * kWarpQ;  // this warp's append buffer
+    uint32_t wn = 0, wpeel = 0;
     uint32_t f_begin = 0;
     uint32_t f_end = (uint32_t)*(volatile unsigned long long*)&ctrl->rc[0];
     uint32_t n_peeled = 0, rounds = 0, nseg = 0;
@@ -752,6 +800,11 @@ __device__ void peel_split(const KParams& P, const uint2* __restrict__ tabS,
         nseg = r;
         for (uint64_t base = f_begin + blockIdx.x * (uint64_t)blockDim.x; base < f_end; base += gstride) {
             const uint64_t f = base + threadIdx.x;
+            bool won = false;
+            uint2 ap[NJ];  // the entries this one appends, by probe
+            bool has[NJ];
+#pragma unroll
+            for (uint32_t j = 0; j < NJ; j++) has[j] = false;
             if (f < f_end) {
                 const uint2 ent = frontier[f];
                 const uint32_t e = ent.x, i = ent.y & 0xffffffu, jp = ent.y >> 24;
@@ -771,33 +824,35 @@ __device__ void peel_split(const KParams& P, const uint2* __restrict__ tabS,
                 const uint32_t bit = 1u << (p & 31);
                 const uint32_t old = atomicOr(claim + (p >> 5), bit);
                 if (!(old & bit)) {
-                    atomicAdd(sh_peeled, 1u);
+                    won = true;
                     const uint32_t dec = 0u - C::one(i);
                     uint32_t rest[NJ];
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
                         if (j == jp) continue;
-                        const uint32_t ev = (mp[j].x << P.log2L) + ((t + map_bias(mp[j])) & (P.L - 1));
-                        rest[j] = atom_add_hint(keys + ev, dec, pl) + dec;
+                        ap[j].x = (mp[j].x << P.log2L) + ((t + map_bias(mp[j])) & (P.L - 1));
+                        rest[j] = atom_add_hint(keys + ap[j].x, dec, pl) + dec;
                     }
                     frontier[f].y = ent.y | 0x80000000u;  // won: replayed by pass 2
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
-                        if (j != jp && C::deg(rest[j]) == 1u)
-                            sh_q[atomicAdd(sh_n, 1u)] =
-                                make_uint2((mp[j].x << P.log2L) + ((t + map_bias(mp[j])) & (P.L - 1)),
-                                           C::low(rest[j]) | (j << 24));
+                        if (j != jp && C::deg(rest[j]) == 1u) {
+                            has[j] = true;
+                            ap[j].y = C::low(rest[j]) | (j << 24);
+                        }
                     }
                 }
             }
-            flush_queue(sh_q, sh_n, sh_base, frontier, f_end, rc);
+            wpeel += __popc(__ballot_sync(0xffffffffu, won));
+#pragma unroll
+            for (uint32_t j = 0; j < NJ; j++) {
+                if (!KT && j >= k) break;
+                wq_push(has[j], ap[j], wbuf, wn, frontier, f_end, rc);
+            }
         }
-        if (threadIdx.x == 0 && *sh_peeled) {
-            atomicAdd(rc, (unsigned long long)*sh_peeled << 32);
-            *sh_peeled = 0;
-        }
+        wq_round_end(wbuf, wn, wpeel, sh_wc, sh_wp, sh_base, frontier, f_end, rc);
         grid.sync();
         const unsigned long long rcv = *(volatile unsigned long long*)rc;
         const uint32_t np = (uint32_t)(rcv >> 32);
@@ -879,6 +934,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     // queue buffer: kPeelThreads * peel_q_per_thread(k) entries of dynamic smem
     extern __shared__ uint2 sh_q[];
     __shared__ uint32_t sh_n, sh_base, sh_peeled;
+    __shared__ uint32_t sh_wc[32], sh_wp[32];
     const uint32_t k = KT ? (uint32_t)KT : P.k;
 
     const uint64_t n_c = *(volatile unsigned long long*)&ctrl->n_cand;
@@ -956,7 +1012,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
         peel_split<KT>(P, tabS, cand, dense, static_cast<uint32_t*>(cells_v),
                        static_cast<float*>(cells_v) + P.c, static_cast<uint32_t*>(cells_v) + 2 * P.c,
                        claim, frontier, ctrl, out_val, out_peeled, stats, n_c, rowoff, vlog, vfill, sh_q,
-                       &sh_n, &sh_base, &sh_peeled);
+                       sh_wc, sh_wp, &sh_base);
     else if (mode == 2)
         peel_body<KT, true>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
                             out_peeled, stats, n_c, rowoff, vlog, vfill, true, sh_q, &sh_n,
@@ -971,8 +1027,9 @@ constexpr uint64_t kSmallPeelCells = 1ull << 20;
 
 // the queue buffer, reused by the finalize as one 4 KB tile (+ 128 B of bits) per warp
 static size_t peel_smem(uint32_t k) {
-    return std::max((size_t)kPeelThreads * peel_q_per_thread(k) * sizeof(uint2),
-                    (size_t)(kPeelThreads / 32) * (kTile + 32) * sizeof(float));
+    return std::max({(size_t)kPeelThreads * peel_q_per_thread(k) * sizeof(uint2),
+                     (size_t)(kPeelThreads / 32) * (kTile + 32) * sizeof(float),
+                     (size_t)(kPeelThreads / 32) * kWarpQ * sizeof(uint2)});
 }
 
 template <int KT>

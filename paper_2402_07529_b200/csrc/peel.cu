@@ -586,7 +586,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                           uint8_t* __restrict__ out_peeled, lhc_stats* stats, uint64_t n_c,
                           const uint32_t* __restrict__ rowoff, uint2* vlog, uint32_t* vfill,
                           bool f0_done, uint2* sh_q, uint32_t* sh_n, uint32_t* sh_base,
-                          uint32_t* sh_peeled) {
+                          uint32_t* sh_wc, uint32_t* sh_wp) {
     using C = Cells<COMPACT>;
     using Cell = typename C::T;
     using K = typename C::K;
@@ -631,6 +631,8 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
     grid.sync();
     if (timer) ctrl->t[3] = globaltimer();
 
+    uint2* wbuf = sh_q + (threadIdx.x >> 5) * kWarpQ;  // this warp's append buffer
+    uint32_t wn = 0, wpeel = 0;
     uint32_t f_begin = 0;
     uint32_t f_end = (uint32_t)*(volatile unsigned long long*)&ctrl->rc[0];
     uint32_t n_peeled = 0, rounds = 0;
@@ -646,6 +648,11 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
         for (uint64_t base = f_begin + blockIdx.x * (uint64_t)blockDim.x; base < f_end;
              base += gstride) {
             const uint64_t f = base + threadIdx.x;
+            bool won = false;
+            uint2 ap[NJ];  // the entries this one appends, by probe
+            bool has[NJ];
+#pragma unroll
+            for (uint32_t j = 0; j < NJ; j++) has[j] = false;
             if (f < f_end) {
                 const uint2 ent = frontier[f];
                 const uint32_t e = ent.x;
@@ -695,7 +702,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                     const uint32_t leader = __ffs(peers) - 1;
                     uint32_t lbase = 0;
                     if (lane == leader) lbase = atomicAdd(vfill + q, (uint32_t)__popc(peers));
-                    atomicAdd(sh_peeled, 1u);
+                    won = true;
                     // all reductions first (independent), then the queue appends
                     const K dec = (K)0 - C::one(COMPACT ? i : p);
                     K rest[NJ];
@@ -712,22 +719,22 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
-                        if (ev[j] != e && C::deg(rest[j]) == 1u)
-                            sh_q[atomicAdd(sh_n, 1u)] =
-                                make_uint2(ev[j], COMPACT ? C::low(rest[j]) | (j << 24) : C::low(rest[j]));
+                        if (ev[j] != e && C::deg(rest[j]) == 1u) {
+                            has[j] = true;
+                            ap[j] = make_uint2(ev[j], COMPACT ? C::low(rest[j]) | (j << 24) : C::low(rest[j]));
+                        }
                     }
                 }
             }
-            if (LHC_PEEL_TIMING && threadIdx.x == 0 && r < kCtrlTimes)
-                atomicMax(&ctrl->tproc[r], globaltimer());
-            flush_queue(sh_q, sh_n, sh_base, frontier, f_end, rc);
-            if (LHC_PEEL_TIMING && threadIdx.x == 0 && r < kCtrlTimes)
-                atomicMax(&ctrl->tflush[r], globaltimer());
+            wpeel += __popc(__ballot_sync(0xffffffffu, won));
+#pragma unroll
+            for (uint32_t j = 0; j < NJ; j++) {
+                if (!KT && j >= k) break;
+                wq_push(has[j], ap[j], wbuf, wn, frontier, f_end, rc);
+            }
         }
-        if (threadIdx.x == 0 && *sh_peeled) {
-            atomicAdd(rc, (unsigned long long)*sh_peeled << 32);
-            *sh_peeled = 0;
-        }
+        if (LHC_PEEL_TIMING && threadIdx.x == 0 && r < kCtrlTimes) atomicMax(&ctrl->tproc[r], globaltimer());
+        wq_round_end(wbuf, wn, wpeel, sh_wc, sh_wp, sh_base, frontier, f_end, rc);
         grid.sync();
         const unsigned long long rcv = *(volatile unsigned long long*)rc;
         const uint32_t np = (uint32_t)(rcv >> 32);
@@ -933,7 +940,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     constexpr uint32_t NJ = KT ? KT : kMaxK;
     // queue buffer: kPeelThreads * peel_q_per_thread(k) entries of dynamic smem
     extern __shared__ uint2 sh_q[];
-    __shared__ uint32_t sh_n, sh_base, sh_peeled;
+    __shared__ uint32_t sh_n, sh_base;
     __shared__ uint32_t sh_wc[32], sh_wp[32];
     const uint32_t k = KT ? (uint32_t)KT : P.k;
 
@@ -950,7 +957,7 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
     const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
-    if (threadIdx.x == 0) { sh_n = 0; sh_peeled = 0; }
+    if (threadIdx.x == 0) sh_n = 0;
     if (timer) ctrl->t[0] = globaltimer();
     if ((mode == 2 || mode == 4) && *(volatile uint32_t*)&ctrl->compact_fail) mode = 0;  // uniform
     if (mode == 3) {  // fallback after the blocked peel: only if a block could not be peeled
@@ -1016,11 +1023,11 @@ k_peel(KParams P, const float* __restrict__ counters, const uint2* __restrict__ 
     else if (mode == 2)
         peel_body<KT, true>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
                             out_peeled, stats, n_c, rowoff, vlog, vfill, true, sh_q, &sh_n,
-                            &sh_base, &sh_peeled);
+                            &sh_base, sh_wc, sh_wp);
     else
         peel_body<KT, false>(P, tabS, cand, dense, cells_v, claim, frontier, ctrl, out_val,
                              out_peeled, stats, n_c, rowoff, vlog, vfill, mode == 1, sh_q, &sh_n,
-                             &sh_base, &sh_peeled);
+                             &sh_base, sh_wc, sh_wp);
 }
 
 constexpr uint64_t kSmallPeelCells = 1ull << 20;

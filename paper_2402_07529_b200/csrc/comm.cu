@@ -296,6 +296,8 @@ __device__ __forceinline__ void fill_shard_nan(float* dense, int q, uint64_t w, 
 template <int G>
 __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
     cg::grid_group grid = cg::this_grid();
+    __shared__ __align__(16) float sh_tile[8][1024];
+    const uint32_t lane = threadIdx.x & 31;
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
     const uint32_t epoch = *(volatile uint32_t*)(A.sig[A.rank] + kEpochSlot);
@@ -310,13 +312,10 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
     const uint64_t nv = n / 4;
     const uint4* src_i = reinterpret_cast<const uint4*>(A.idx);
     const uint4* src_v = reinterpret_cast<const uint4*>(A.val);
-    // the first half of the grid pushes over NVLink while the second half zeroes
-    // the local dense ranges in HBM (the two transfers overlap)
-    const uint32_t half = gridDim.x / 2;
-    const bool pusher = blockIdx.x < half || half == 0;
-    const uint64_t rtid = (pusher ? blockIdx.x : blockIdx.x - half) * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t rstride = (uint64_t)(half ? half : gridDim.x) * blockDim.x;
-    if (pusher) {
+    // the whole grid pushes over NVLink; the peers' ranges of the local dense output are
+    // assembled chunk by chunk after the barrier (no zeroing pass, no scattered stores)
+    const uint64_t rtid = gtid, rstride = gstride;
+    {
 #pragma unroll 1
         for (int dd = 1; dd < G; dd++) {
             const int q = (A.rank + dd) % G;
@@ -336,17 +335,6 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
                 A.sig[q][kGatherCountSlot + par * kMaxRanks + A.rank] = own_over ? kOverflowMark : (uint32_t)n;
         }
     }
-    if (!pusher || half == 0) {
-        // zero the peers' shard ranges [0, lo) and [hi, d) of the local dense output
-        // (lo, hi multiples of 4 unless hi = d)
-        const uint64_t lo = (uint64_t)A.rank * A.shard_width;
-        const uint64_t hi = min((uint64_t)A.d, lo + A.shard_width);
-        float4* d4 = reinterpret_cast<float4*>(A.dense);
-        const uint64_t a4 = lo / 4, b4 = hi / 4, e4 = A.d / 4, own4 = b4 - a4;
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (uint64_t u = rtid; u < e4 - own4; u += rstride) __stcs(d4 + (u < a4 ? u : u + own4), z);
-        for (uint64_t i = max(hi, 4 * e4) + rtid; i < A.d; i += rstride) A.dense[i] = 0.f;
-    }
     sh_barrier<G>(grid, A, epoch + 1);
     if (own_over) fill_shard_nan(A.dense, A.rank, A.shard_width, A.d, gtid, gstride);
 #pragma unroll 1
@@ -359,19 +347,54 @@ __global__ void __launch_bounds__(256) k_allgather_decoded(ShArgs A) {
         }
         const uint64_t nq = min((uint64_t)cnt, A.cap);
         const uint32_t* slot = reinterpret_cast<const uint32_t*>(A.gather[A.rank] + ((uint64_t)par * G + q) * A.cap);
-        const uint4* si = reinterpret_cast<const uint4*>(slot);
-        const uint4* sv = reinterpret_cast<const uint4*>(slot + A.cap);
-        float* base = A.dense + (uint64_t)q * A.shard_width;
-        for (uint64_t u = gtid; u < nq / 4; u += gstride) {
-            const uint4 a = __ldcs(si + u), b = __ldcs(sv + u);
-            if (b.x) base[a.x] = __uint_as_float(b.x);
-            if (b.y) base[a.y] = __uint_as_float(b.y);
-            if (b.z) base[a.z] = __uint_as_float(b.z);
-            if (b.w) base[a.w] = __uint_as_float(b.w);
-        }
-        for (uint64_t i = (nq & ~3ull) + gtid; i < nq; i += gstride) {
-            const uint32_t v = slot[A.cap + i];
-            if (v) base[slot[i]] = __uint_as_float(v);
+        const uint32_t* si = slot;
+        const float* sv = reinterpret_cast<const float*>(slot + A.cap);
+        // shard q = coordinates [q w, min(d, (q + 1) w)), its list ascending in
+        // shard-local coordinates: a warp assembles a contiguous range of its
+        // 1024-coordinate chunks in shared memory (zeros + the listed values) and
+        // writes each chunk with full-line stores
+        const uint64_t s0 = (uint64_t)q * A.shard_width;
+        const uint64_t len = s0 < A.d ? min((uint64_t)A.shard_width, (uint64_t)A.d - s0) : 0;
+        const uint64_t nch = (len + 1023) / 1024;
+        const uint64_t nwarps = gstride >> 5, wid = gtid >> 5;
+        const uint64_t cpw = (nch + nwarps - 1) / nwarps;
+        const uint64_t c0 = min(nch, wid * cpw), c1 = min(nch, c0 + cpw);
+        if (c0 < c1) {
+            // first list entry of chunk c0 (binary search, every lane the same)
+            uint64_t lo = 0, hi = nq;
+            const uint64_t key = c0 * 1024;
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) / 2;
+                if (__ldcs(si + mid) < key) lo = mid + 1; else hi = mid;
+            }
+            uint64_t pos = lo;
+            float* tile = sh_tile[threadIdx.x >> 5];
+            float4* t4 = reinterpret_cast<float4*>(tile);
+            for (uint64_t c = c0; c < c1; c++) {
+#pragma unroll
+                for (int u = 0; u < 8; u++) t4[lane + 32 * u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                __syncwarp();
+                const uint64_t cend = (c + 1) * 1024;
+                for (;;) {
+                    const uint64_t a = pos + lane;
+                    const uint32_t ix = a < nq ? __ldcs(si + a) : 0xffffffffu;
+                    const bool in = a < nq && ix < cend;
+                    if (in) tile[ix & 1023] = __ldcs(sv + a);
+                    const uint32_t nin = __popc(__ballot_sync(0xffffffffu, in));  // a prefix: sorted
+                    pos += nin;
+                    if (nin < 32) break;
+                }
+                __syncwarp();
+                float* out = A.dense + s0 + c * 1024;
+                if ((c + 1) * 1024 <= len) {
+                    float4* o4 = reinterpret_cast<float4*>(out);
+#pragma unroll
+                    for (int u = 0; u < 8; u++) __stcs(o4 + lane + 32 * u, t4[lane + 32 * u]);
+                } else {
+                    for (uint64_t a = lane; c * 1024 + a < len; a += 32) out[a] = tile[a];
+                }
+                __syncwarp();
+            }
         }
     }
     // every block read epoch / par before the barrier's grid syncs

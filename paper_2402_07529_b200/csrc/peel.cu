@@ -260,18 +260,6 @@ __global__ void __launch_bounds__(1024) k_pair_scan(uint32_t* dst_off, uint32_t 
     block_excl_scan(dst_off, n, sh);
 }
 
-// the same scan staged in shared memory (coalesced load and store) when the offsets
-// fit: the global version is latency-bound (VGG19, 15.7 K offsets: 18 us)
-constexpr uint32_t kPairScanSmemMax = 48 * 1024;
-__global__ void __launch_bounds__(1024) k_pair_scan_smem(uint32_t* dst_off, uint32_t n) {
-    extern __shared__ uint32_t sh_off[];
-    __shared__ uint32_t sh[32];
-    for (uint32_t a = threadIdx.x; a < n; a += blockDim.x) sh_off[a] = dst_off[a];
-    __syncthreads();
-    block_excl_scan(sh_off, n, sh);
-    __syncthreads();
-    for (uint32_t a = threadIdx.x; a < n; a += blockDim.x) dst_off[a] = sh_off[a];
-}
 
 __global__ void __launch_bounds__(256) k_pair_scatter(KParams P, const uint2* __restrict__ tabS,
                                                       const uint32_t* __restrict__ dst_off,
@@ -425,19 +413,7 @@ void launch_pair_lists(const KParams& P, const uint2* tabS, uint32_t* dst_off, u
     const uint32_t gp = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((npairs + 255) / 256, (uint64_t)num_sms() * 8));
     cudaMemsetAsync(dst_off, 0, (nD + 1) * sizeof(uint32_t), s);
     k_pair_count<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos);
-    if (nD + 1 <= kPairScanSmemMax) {
-        static bool attr[64] = {};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev >= 64 || !attr[dev]) {
-            cudaFuncSetAttribute(k_pair_scan_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(kPairScanSmemMax * sizeof(uint32_t)));
-            if (dev < 64) attr[dev] = true;
-        }
-        k_pair_scan_smem<<<1, 1024, (nD + 1) * sizeof(uint32_t), s>>>(dst_off, (uint32_t)nD + 1);
-    } else {
-        k_pair_scan<<<1, 1024, 0, s>>>(dst_off, (uint32_t)nD + 1);
-    }
+    k_pair_scan<<<1, 1024, 0, s>>>(dst_off, (uint32_t)nD + 1);
     k_pair_scatter<<<gp, 256, 0, s>>>(P, tabS, dst_off, pair_pos, dst_list);
     count_launch(3);
 }

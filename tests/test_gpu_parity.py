@@ -607,6 +607,37 @@ def test_compress_batch_chained_and_repeated(lhc, ora):
         assert np.array_equal(F(sks[r].counters), Y)
 
 
+@pytest.mark.parametrize("k,kb,L", [(3, 3, 1024), (4, 5, 1024), (3, 3, 256), (2, 1, 32)])
+def test_compress_rows_ragged_one_sketch(lhc, ora, k, kb, L):
+    """The row-major batched compress (every input into one sketch: a warp takes chunk
+    row r of each input in turn; compile-time k = k_B = 3 or run-time k, k_B) with
+    inputs of different lengths — one ending mid-chunk, one many chunks short, one
+    shorter than a chunk — equals the oracle's per-input compressions accumulated
+    (homomorphism, P:L137)."""
+    d = 50_000
+    ds = [d, d - 97, d - 2048 - 5, 1000, d - 1]
+    W = len(ds)
+    s = lhc.size_workload(d, 0.02, W, L=L)
+    m = kb * L * max(1, s.m // (kb * L))
+    c = k * L * max(1, s.c // (k * L))
+    p = gpu_params(lhc, d, m, c, k=k, kb=kb, L=L, seed=0x5EED + k)
+    xs = make_workers(d, 1000, W, 9, "dyadic")
+    sk = lhc.Sketch(p)
+    sk.clear()
+    lhc.sketch_compress_batch(p, [torch.from_numpy(x).cuda() for x in xs],
+                              [sk.bitmap] * W, [sk.counters] * W, ds=ds)
+    torch.cuda.synchronize()
+    op = ora_params(ora, p)
+    parts = []
+    for x, dd in zip(xs, ds):
+        x = x.copy()
+        x[dd:] = 0.0
+        parts.append(ora.compress_dense(op, x))
+    B, Y = ora.aggregate([a for a, _ in parts], [b for _, b in parts])
+    assert np.array_equal(U(sk.bitmap), B)
+    assert np.array_equal(F(sk.counters), Y)
+
+
 # ------------------------------- generic k / k_B (run-time k kernels, NEXT-4) --
 
 @pytest.mark.parametrize("k,kb", [(2, 1), (4, 5), (3, 7), (5, 0)])

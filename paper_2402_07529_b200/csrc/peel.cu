@@ -178,6 +178,21 @@ __device__ __forceinline__ uint32_t atom_add_hint(uint32_t* a, uint32_t v, uint6
     return old;
 }
 
+// The frontier queue and the value log are streamed (written once, read once a round
+// or a phase later): evict-first so that they do not push the decode state out of L2.
+#ifndef LHC_STREAM_QUEUE
+#define LHC_STREAM_QUEUE 1
+#endif
+template <typename T>
+__device__ __forceinline__ void st_stream(T* a, T v) {
+    if (LHC_STREAM_QUEUE) __stcs(a, v); else *a = v;
+}
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* a) {
+    if (LHC_STREAM_QUEUE) return __ldcs(a);
+    return *a;
+}
+
 // Block-aggregated append of the pairs in sh_q to the queue segment that starts
 // at seg_base, through the low half of the round's counter rc.
 __device__ __forceinline__ void flush_queue(uint2* sh_q, uint32_t* sh_n, uint32_t* sh_base,
@@ -205,7 +220,7 @@ __device__ __forceinline__ void wq_push(bool has, uint2 v, uint2* wbuf, uint32_t
         uint32_t b = 0;
         if (lane == 0) b = (uint32_t)atomicAdd(rc, (unsigned long long)wn);
         b = __shfl_sync(0xffffffffu, b, 0) + seg_base;
-        for (uint32_t a = lane; a < wn; a += 32) frontier[b + a] = wbuf[a];
+        for (uint32_t a = lane; a < wn; a += 32) st_stream(frontier + b + a, wbuf[a]);
         __syncwarp();
         wn = 0;
     }
@@ -233,7 +248,7 @@ __device__ __forceinline__ void wq_round_end(uint2* wbuf, uint32_t& wn, uint32_t
     }
     __syncthreads();
     const uint32_t b = *sh_base + sh_wc[warp];
-    for (uint32_t a = lane; a < wn; a += 32) frontier[b + a] = wbuf[a];
+    for (uint32_t a = lane; a < wn; a += 32) st_stream(frontier + b + a, wbuf[a]);
     wn = 0;
     wpeel = 0;
 }
@@ -655,7 +670,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
 #pragma unroll
             for (uint32_t j = 0; j < NJ; j++) has[j] = false;
             if (f < f_end) {
-                const uint2 ent = frontier[f];
+                const uint2 ent = ld_stream(frontier + f);
                 const uint32_t e = ent.x;
                 // issued back to back (volatile loads are not sunk into the branch): the
                 // pure cell's residual, the row maps of the candidate's input row and the
@@ -716,7 +731,7 @@ __device__ void peel_body(const KParams& P, const uint2* __restrict__ tabS,
                         rest[j] = atom_add_hint(&cells[ev[j]].key, dec, pl) + dec;
                     }
                     lbase = __shfl_sync(peers, lbase, leader) + __popc(peers & ((1u << lane) - 1u));
-                    vlog[lbase] = make_uint2(p, __float_as_uint(val));
+                    st_stream(vlog + lbase, make_uint2(p, __float_as_uint(val)));
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
@@ -814,7 +829,7 @@ __device__ void peel_split(const KParams& P, const uint2* __restrict__ tabS,
 #pragma unroll
             for (uint32_t j = 0; j < NJ; j++) has[j] = false;
             if (f < f_end) {
-                const uint2 ent = frontier[f];
+                const uint2 ent = ld_stream(frontier + f);
                 const uint32_t e = ent.x, i = ent.y & 0xffffffu, jp = ent.y >> 24;
                 const uint2* row = tabS + (uint64_t)i * k;
                 uint2 mp[NJ];
@@ -842,7 +857,7 @@ __device__ void peel_split(const KParams& P, const uint2* __restrict__ tabS,
                         ap[j].x = (mp[j].x << P.log2L) + ((t + map_bias(mp[j])) & (P.L - 1));
                         rest[j] = atom_add_hint(keys + ap[j].x, dec, pl) + dec;
                     }
-                    frontier[f].y = ent.y | 0x80000000u;  // won: replayed by pass 2
+                    st_stream(&frontier[f].y, ent.y | 0x80000000u);  // won: replayed by pass 2
 #pragma unroll
                     for (uint32_t j = 0; j < NJ; j++) {
                         if (!KT && j >= k) break;
@@ -909,7 +924,7 @@ __device__ void peel_split(const KParams& P, const uint2* __restrict__ tabS,
                              -map_sign(mp[j]) * val, pl);
             }
             lbase = __shfl_sync(peers, lbase, leader) + __popc(peers & ((1u << lane) - 1u));
-            vlog[lbase] = make_uint2(p, __float_as_uint(val));
+            st_stream(vlog + lbase, make_uint2(p, __float_as_uint(val)));
         }
         grid.sync();
     }

@@ -642,10 +642,14 @@ def test_compress_rows_ragged_one_sketch(lhc, ora, k, kb, L):
 
 @pytest.mark.parametrize("k,kb", [(2, 1), (4, 5), (3, 7), (5, 0)])
 @pytest.mark.parametrize("law", ["dyadic", "gauss"])
-def test_generic_k_and_probes(lhc, ora, k, kb, law):
+@pytest.mark.parametrize("build", ["default", "split"])
+def test_generic_k_and_probes(lhc, ora, k, kb, law, build, monkeypatch):
     """The run-time-k kernels (k != 3 or k_B != 3): bitmaps, candidates, flags and
     rounds exact, values exact/tol — including k = 2 below its peeling threshold,
-    where most values come from the median (here: mean) fallback."""
+    where most values come from the median (here: mean) fallback; also through the
+    two-pass peel of the split state (run-time k)."""
+    if build != "default":
+        monkeypatch.setenv("LHC_CELL_BUILD", build)
     d, nnz, W = 300_000, 6_000, 2
     s = lhc.size_workload(d, nnz / d, W, k=k, k_bloom=kb)
     p = gpu_params(lhc, d, s.m, s.c, k=k, kb=kb, seed=0x6E + 16 * k + kb)

@@ -78,8 +78,12 @@ CASES = [
 
 
 @pytest.mark.parametrize("d,nnz,W,L,k,blocks,gamma", CASES)
-@pytest.mark.parametrize("decode", ["default", "deterministic"])
-def test_guard_bands_intact(lhc, ora, d, nnz, W, L, k, blocks, gamma, decode):
+@pytest.mark.parametrize("decode", ["default", "deterministic", "split"])
+def test_guard_bands_intact(lhc, ora, d, nnz, W, L, k, blocks, gamma, decode, monkeypatch):
+    if decode == "split":  # the two-pass peel of the split state (forced at these sizes)
+        if blocks:
+            pytest.skip("the blocked sketch is peeled block-locally")
+        monkeypatch.setenv("LHC_CELL_BUILD", "split")
     s = lhc.size_workload(d, nnz / d, W, L=L, k=k, gamma=gamma)
     c = s.c
     if blocks:
@@ -106,6 +110,10 @@ def test_guard_bands_intact(lhc, ora, d, nnz, W, L, k, blocks, gamma, decode):
     B = g(words, torch.int32, 0)
     Y = g(cells, torch.float32, 0.0)
     lhc.sketch_aggregate(p, bms, cts, B, Y)
+    # row-major batched compress of all workers into one sketch (k_compress_rows)
+    B3 = g(words, torch.int32, 0)
+    Y3 = g(cells, torch.float32, 0.0)
+    lhc.sketch_compress_batch(p, xin, [B3] * W, [Y3] * W)
     # COO compress of the same gradients into another sketch (plus out-of-range entries)
     B2 = g(words, torch.int32, 0)
     Y2 = g(cells, torch.float32, 0.0)
@@ -132,6 +140,8 @@ def test_guard_bands_intact(lhc, ora, d, nnz, W, L, k, blocks, gamma, decode):
     assert g.intact(), "a kernel wrote outside its buffer"
     assert int(bad.item()) == 2 * W
     assert np.array_equal(B.cpu().numpy().view(np.uint32), B2.cpu().numpy().view(np.uint32))
+    assert np.array_equal(B.cpu().numpy().view(np.uint32), B3.cpu().numpy().view(np.uint32))
+    assert np.array_equal(Y.cpu().numpy(), Y3.cpu().numpy())  # dyadic sums: exact in any order
     st = lhc.read_stats(stats)
     n = st["n_cand"]
     assert n == ref.stats.n_cand and st["rounds"] == ref.stats.rounds

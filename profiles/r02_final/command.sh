@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/final3; mkdir -p $O
+O=gpurun_out/final4; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $O/gpu.txt
 lscpu > $O/lscpu.txt 2>&1
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/tests_gpu.txt 2>&1; echo "rc=$?" >> $O/tests_gpu.txt

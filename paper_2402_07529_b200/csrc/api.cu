@@ -228,10 +228,12 @@ static void compress_batches(const KParams& P, int n, const float* const* xs, co
         B.start[B.n] = start;
         bool same = B.n > 1;
         for (uint32_t b = 1; b < B.n; b++) same &= B.d[b] == B.d[0];
-        // interleave the inputs row by row when their sketch is well beyond L2 (then
-        // the lines a row's reductions touch are reused by the other inputs before
-        // they are evicted; measured: BERT 10 %, 387 MB sketch, 3.04 -> 2.02 ms);
-        // otherwise the input-major order streams each input once (VGG: 1.09 vs 1.14 ms)
+        // (input-major kernel only, i.e. inputs into several sketches: the one-sketch
+        // case takes the row-major kernel, compress.cu) interleave the inputs row by
+        // row when their sketch is well beyond L2 (then the lines a row's reductions
+        // touch are reused by the other inputs before they are evicted; measured:
+        // BERT 10 %, 387 MB sketch, 3.04 -> 2.02 ms); otherwise the input-major order
+        // streams each input once (VGG: 1.09 vs 1.14 ms)
         const size_t sketch = (size_t)P.m / 8 + (size_t)P.c * 4;
         bool inter = same && sketch > (size_t)l2_bytes() * 3 / 2;
         if (const char* ev = getenv("LHC_COMPRESS_INTERLEAVE")) inter = same && strcmp(ev, "0") != 0;

@@ -33,7 +33,10 @@ void launch_hash_rows(const KParams& P, uint32_t dom, uint64_t n_rows, uint2* ou
 }
 
 // ---------------------------------------------------------------------------
-// Dense compression.
+// Dense compression: two kernels with the same per-chunk work and different chunk
+// orders — k_compress_rows (below; every input into one sketch: chunk row r of every
+// input in turn, row maps hashed once per chunk row) and k_compress_dense (input
+// after input; inputs into several sketches, e.g. per-worker sketches).
 //
 // One warp owns a chunk of 1024 consecutive coordinates at a time (1024/L input
 // rows) and needs no block-level synchronisation:

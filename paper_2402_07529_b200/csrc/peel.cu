@@ -34,8 +34,11 @@
 // it is appended as (coordinate, value) to its chunk's segment of a log whose
 // segments start at the chunk's first candidate slot (the query's row offsets), so
 // the appends of a chunk fill whole lines and the finalize reads them back in order.
-// Queue appends are aggregated per CTA in shared memory (one global atomic per
-// CTA per pass); every cell enters the queue at most once (c entries).
+// Queue appends go to warp-private shared-memory buffers (no block barrier inside a
+// round; one global reservation per CTA and round, or per full buffer); every cell
+// enters the queue at most once (c entries).  When the 8-byte state exceeds the L2
+// but its 4-byte key array fits, the rounds run in two passes over a split state
+// (peel_split: keys first, then the residuals replayed segment by segment).
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>

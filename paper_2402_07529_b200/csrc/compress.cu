@@ -60,13 +60,18 @@ void launch_hash_rows(const KParams& P, uint32_t dom, uint64_t n_rows, uint2* ou
 // gradient does not evict the sketch lines they accumulate into.
 // ---------------------------------------------------------------------------
 #ifndef LHC_COMPRESS_WARPS
-#define LHC_COMPRESS_WARPS 12  // one 12-warp CTA per SM (VGG19 compress 934 -> 865 us vs two 8-warp CTAs)
+#define LHC_COMPRESS_WARPS 8  // input-major kernel: two 8-warp CTAs per SM
 #endif
 #ifndef LHC_COMPRESS_STAGES
 #define LHC_COMPRESS_STAGES 2
 #endif
 constexpr int kCompressWarps = LHC_COMPRESS_WARPS;
 constexpr int kCompressThreads = kCompressWarps * 32;
+#ifndef LHC_ROWS_WARPS
+#define LHC_ROWS_WARPS 12  // row-major kernel: one 12-warp CTA per SM (VGG19 934 -> 865 us vs two 8-warp CTAs)
+#endif
+constexpr int kRowsWarps = LHC_ROWS_WARPS;
+constexpr int kRowsThreads = kRowsWarps * 32;
 constexpr int kStages = LHC_COMPRESS_STAGES;
 constexpr uint32_t kFullMask = 0xffffffffu;
 
@@ -306,7 +311,7 @@ k_compress_dense(KParams P, const __grid_constant__ CompressBatch B,
 // lane: lane-serial over each lane's word when the words are sparse, warp-cooperative
 // over the nonzero words when a few are dense.
 template <int KT, int KBT>
-__global__ void __launch_bounds__(kCompressThreads)
+__global__ void __launch_bounds__(kRowsThreads)
 k_compress_rows(KParams P, const __grid_constant__ CompressBatch B, uint64_t nrc,
                 unsigned long long* __restrict__ nnz_out) {
     extern __shared__ __align__(128) unsigned char sh_all[];
@@ -322,8 +327,8 @@ k_compress_rows(KParams P, const __grid_constant__ CompressBatch B, uint64_t nrc
     uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sh_map) +
                                                 ((n_map * 8 + 15) / 16) * 16);
     const uint32_t n = B.n;
-    const uint64_t stride = (uint64_t)gridDim.x * kCompressWarps;
-    const uint64_t first = blockIdx.x * (uint64_t)kCompressWarps + warp;
+    const uint64_t stride = (uint64_t)gridDim.x * kRowsWarps;
+    const uint64_t first = blockIdx.x * (uint64_t)kRowsWarps + warp;
     uint64_t pol_keep, pol_stream;
     {
         uint64_t pol_norm;
@@ -464,8 +469,6 @@ void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned lo
                            cudaStream_t s) {
     const uint64_t nchunks = B.start[B.n];
     const uint32_t n_map = (kTile >> P.log2L) * (P.k + P.kb);
-    const size_t smem = kCompressWarps * compress_warp_smem(n_map);
-    const size_t smax = kCompressWarps * compress_warp_smem(32 * 2 * kMaxK);
     // (LHC_COMPRESS_IMPL=chunks: the input-major kernel, one chunk of one input per unit)
     static const bool env_chunks = [] {
         const char* e = getenv("LHC_COMPRESS_IMPL");
@@ -479,6 +482,12 @@ void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned lo
     bool one_sketch = true;
     for (uint32_t b = 1; b < B.n; b++) one_sketch &= B.counters[b] == B.counters[0] && B.bitmap[b] == B.bitmap[0];
     if (!one_sketch) by_chunks = true;
+    // warps per CTA: 8 for the input-major kernel, 12 for the row-major one (the
+    // sharded decode's (worker, shard) batches take the input-major kernel and were
+    // 15 % slower at 12)
+    const int warps = by_chunks ? kCompressWarps : kRowsWarps;
+    const size_t smem = warps * compress_warp_smem(n_map);
+    const size_t smax = warps * compress_warp_smem(32 * 2 * kMaxK);
     const void* fn = by_chunks ? (const void*)k_compress_dense
                      : fast    ? (const void*)k_compress_rows<3, 3>
                                : (const void*)k_compress_rows<0, 0>;
@@ -490,10 +499,10 @@ void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned lo
     if (dev < 64 && !per_sm[dev][fi][key]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
         int nb = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kCompressThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, warps * 32, smem);
         per_sm[dev][fi][key] = std::max(1, nb);
     }
-    const int resident = dev < 64 ? per_sm[dev][fi][key] : 2;
+    const int resident = dev < 64 ? per_sm[dev][fi][key] : 1;
     if (by_chunks) {
         const uint32_t blocks = (uint32_t)std::min<uint64_t>((nchunks + kCompressWarps - 1) / kCompressWarps,
                                                              (uint64_t)num_sms() * resident);
@@ -501,12 +510,12 @@ void launch_compress_dense(const KParams& P, const CompressBatch& B, unsigned lo
     } else {
         uint64_t nrc = 0;  // chunk rows: the longest input's chunks
         for (uint32_t b = 0; b < B.n; b++) nrc = std::max<uint64_t>(nrc, B.start[b + 1] - B.start[b]);
-        const uint32_t blocks = (uint32_t)std::min<uint64_t>((nrc + kCompressWarps - 1) / kCompressWarps,
+        const uint32_t blocks = (uint32_t)std::min<uint64_t>((nrc + kRowsWarps - 1) / kRowsWarps,
                                                              (uint64_t)num_sms() * resident);
         if (fast)
-            k_compress_rows<3, 3><<<blocks, kCompressThreads, smem, s>>>(P, B, nrc, nnz_out);
+            k_compress_rows<3, 3><<<blocks, kRowsThreads, smem, s>>>(P, B, nrc, nnz_out);
         else
-            k_compress_rows<0, 0><<<blocks, kCompressThreads, smem, s>>>(P, B, nrc, nnz_out);
+            k_compress_rows<0, 0><<<blocks, kRowsThreads, smem, s>>>(P, B, nrc, nnz_out);
     }
     count_launch();
 }
